@@ -1,0 +1,710 @@
+// Device engine: plan compilation, arena management, the layer scheduler and
+// the C-ABI entry points that replace run_sequential / run_parallel /
+// evaluate (proj/src/executor.cpp:168-276).
+//
+// Execution model. One grid launch per dependency level replaces the
+// reference's barrier-per-phase thread pool (executor.cpp:185-231): conv
+// layers, then the TermScale phase, then addition layers, then extraction.
+// The launch sequence for a batch size is captured once into a CUDA graph
+// and replayed, so a whole evaluation is a single graph launch.
+//
+// Plan-time rewrites (results stay bit-identical):
+//  * In-place convolutions (the coefficient fold b_{n-2} := b_{n-2} * a,
+//    jobgraph.cpp:115) are made out-of-place by versioning the slot: the
+//    earlier job that produced the pre-fold value writes a scratch slot that
+//    the fold (and any reader in between) reads instead. Every thread can
+//    then stream its own coefficients without a block-wide input copy.
+//  * Exponent folding (fold_exponents, jobgraph.cpp:168-197) becomes device
+//    conv jobs in prologue layers (pse_evaluate only).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host_graph.hpp"
+#include "kernels.cuh"
+
+namespace pse {
+namespace {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct ConvRow {
+  int64_t in1, in2, out;
+  uint8_t copy;
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::invalid_argument& e) {
+    set_error(e.what());
+    return PSE_EINVAL;
+  } catch (const CudaError& e) {
+    set_error(e.what());
+    return PSE_ECUDA;
+  } catch (const std::bad_alloc&) {
+    set_error("out of host memory");
+    return PSE_ENOMEM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return PSE_ESTATE;
+  }
+}
+
+// stage: reference-layout static block [q][b][top][d+1] -> arena
+__global__ void k_stage(const double* __restrict__ in, double* __restrict__ arena, Geom G, int64_t top, int batch,
+                        int64_t in_point_words) {
+  const int d1 = G.d + 1;
+  const int64_t n = static_cast<int64_t>(G.Q) * batch * top * d1;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(t % d1);
+    int64_t r = t / d1;
+    const int64_t s = r % top;
+    r /= top;
+    const int64_t b = r % batch;
+    const int q = static_cast<int>(r / batch);
+    arena[b * G.point_words + s * G.slot_words + static_cast<int64_t>(q) * G.S + j] =
+        in[(static_cast<int64_t>(q) * batch + b) * in_point_words + s * d1 + j];
+  }
+}
+
+// arena -> reference DataArray layout [q][b][TS][d+1]
+__global__ void k_export(const double* __restrict__ arena, double* __restrict__ out, Geom G, int64_t TS, int batch) {
+  const int d1 = G.d + 1;
+  const int64_t n = static_cast<int64_t>(G.Q) * batch * TS * d1;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(t % d1);
+    int64_t r = t / d1;
+    const int64_t s = r % TS;
+    r /= TS;
+    const int64_t b = r % batch;
+    const int q = static_cast<int>(r / batch);
+    out[t] = arena[b * G.point_words + s * G.slot_words + static_cast<int64_t>(q) * G.S + j];
+  }
+}
+
+unsigned grid_for(int64_t n, int threads, int sms) {
+  const int64_t need = (n + threads - 1) / threads;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(need, int64_t(sms) * 32)));
+}
+
+template <class T>
+T* dev_alloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) return nullptr;
+  ck(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+template <class T>
+T* dev_upload(const std::vector<T>& v, cudaStream_t s) {
+  T* p = dev_alloc<T>(v.size());
+  if (p) ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "upload");
+  return p;
+}
+
+}  // namespace
+
+struct Plan {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;
+  int n = 0, N = 0, d = 0, m = 1, mode = 0, P = 1, Q = 1;
+  int64_t TS = 0, TSdev = 0, top = 0;
+  int max_batch = 1;
+  Geom G{};
+  const Launchers* L = nullptr;
+  // layer job tables on the device
+  std::vector<std::pair<int4*, int>> conv_layers;  // (jobs, njobs)
+  std::vector<std::pair<int2*, int>> add_layers;
+  int2* ts = nullptr;
+  int nts = 0;
+  int* row_slot = nullptr;
+  int* row_mult = nullptr;
+  int nrows = 0;
+  std::vector<void*> owned;
+  // buffers
+  double* arena = nullptr;
+  double* stage = nullptr;  // [Q][max_batch][top][d+1]
+  double* vg = nullptr;     // [Q][max_batch][n+1][d+1]
+  double* dyn = nullptr;    // lazily: [Q][max_batch][TS][d+1]
+  // accounting (per point)
+  int64_t flops_model = 0, alg_ops = 0, conv_jobs = 0, add_jobs = 0, copy_jobs = 0;
+  std::map<int, cudaGraphExec_t> graphs;
+  std::vector<cudaEvent_t> ev;
+
+  ~Plan() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& [b, g] : graphs) cudaGraphExecDestroy(g);
+    for (cudaEvent_t x : ev) cudaEventDestroy(x);
+    for (void* p : owned) cudaFree(p);
+    cudaFree(arena);
+    cudaFree(stage);
+    cudaFree(vg);
+    cudaFree(dyn);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  // launch the whole phase sequence; if ts is non-null, record an event
+  // after every phase into ts (conv layers, scale, add layers, extract)
+  int launch_all(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
+    int launches = 0;
+    for (auto& [jobs, nj] : conv_layers) {
+      ConvArgs a{arena, G, jobs, nj, (d + 2) / 2, batch};
+      L->conv(a, stream);
+      ++launches;
+      if (marks) mark(marks, 'c');
+    }
+    if (nts) {
+      ScaleArgs a{arena, G, ts, nts, batch};
+      L->scale(a, stream);
+      ++launches;
+      if (marks) mark(marks, 's');
+    }
+    for (auto& [jobs, nj] : add_layers) {
+      AddArgs a{arena, G, jobs, nj, batch};
+      L->add(a, stream);
+      ++launches;
+      if (marks) mark(marks, 'a');
+    }
+    ExtractArgs e{arena, G, row_slot, row_mult, nrows, batch, vg};
+    L->extract(e, stream);
+    ++launches;
+    if (marks) mark(marks, 'e');
+    return launches;
+  }
+
+  void mark(std::vector<std::pair<char, cudaEvent_t>>* marks, char kind) {
+    const size_t i = marks->size();
+    ensure_events(static_cast<int>(i) + 2);
+    ck(cudaEventRecord(ev[i + 1], stream), "event");
+    marks->emplace_back(kind, ev[i + 1]);
+  }
+
+  void ensure_events(int k) {
+    while (static_cast<int>(ev.size()) < k) {
+      cudaEvent_t x;
+      ck(cudaEventCreate(&x), "event create");
+      ev.push_back(x);
+    }
+  }
+
+  int phase_count() const {
+    return static_cast<int>(conv_layers.size()) + (nts ? 1 : 0) + static_cast<int>(add_layers.size()) + 1;
+  }
+};
+
+namespace {
+
+// Build the device plan: validate, version in-place slots, add optional
+// prologue (fold) jobs, upload job tables, allocate the arena.
+Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::vector<std::vector<ConvRow>>& prologue,
+                 int64_t prologue_slots) {
+  if (!valid_precision(g.m)) throw std::invalid_argument("unsupported precision level");
+  if (g.mode != PSE_MODE_REAL && g.mode != PSE_MODE_COMPLEX) throw std::invalid_argument("unsupported mode");
+  if (max_batch < 1) throw std::invalid_argument("max_batch must be at least 1");
+  const std::string why = validate_desc(g);
+  if (!why.empty()) throw std::invalid_argument("invalid job graph: " + why);
+  if (g.total_slots + prologue_slots + g.conv_layer_off[g.n_conv_layers] >= (int64_t(1) << 31))
+    throw std::invalid_argument("graph too large for 32-bit slot indices");
+
+  std::unique_ptr<Plan> p(new Plan);
+  p->device = device;
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  ck(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device), "attr");
+  ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "stream");
+  p->n = g.n;
+  p->N = g.N;
+  p->d = g.d;
+  p->m = g.m;
+  p->mode = g.mode;
+  p->P = g.mode == PSE_MODE_COMPLEX ? 2 : 1;
+  p->Q = p->P * g.m;
+  p->TS = g.total_slots;
+  p->top = 1 + static_cast<int64_t>(g.N) + g.n;
+  p->max_batch = max_batch;
+  p->L = launchers_for(g.m, g.mode == PSE_MODE_COMPLEX);
+  p->L->prepare();
+
+  // conv rows per layer: prologue layers first, then the graph's layers
+  std::vector<std::vector<ConvRow>> layers = prologue;
+  for (int32_t L = 0; L < g.n_conv_layers; ++L) {
+    std::vector<ConvRow> rows;
+    for (int64_t t = g.conv_layer_off[L]; t < g.conv_layer_off[L + 1]; ++t) {
+      rows.push_back({g.conv_in1[t], g.conv_in2[t], g.conv_out[t], g.conv_copy[t]});
+      if (g.conv_copy[t]) ++p->copy_jobs;
+    }
+    layers.push_back(std::move(rows));
+  }
+  int64_t next_slot = g.total_slots + prologue_slots;
+  // version in-place slots (out == in1, not a copy)
+  std::map<int64_t, std::pair<size_t, size_t>> last_writer;  // slot -> (layer, row)
+  for (size_t L = 0; L < layers.size(); ++L) {
+    for (size_t r = 0; r < layers[L].size(); ++r) {
+      ConvRow& j = layers[L][r];
+      if (j.copy || j.out != j.in1) continue;
+      auto it = last_writer.find(j.in1);
+      if (it == last_writer.end()) throw std::invalid_argument("in-place job on a slot without an earlier writer");
+      const int64_t s = j.in1, scratch = next_slot++;
+      const size_t Lw = it->second.first;
+      layers[Lw][it->second.second].out = scratch;
+      for (size_t L2 = Lw + 1; L2 <= L; ++L2)
+        for (ConvRow& q : layers[L2]) {
+          if (&q != &j && q.out == s && L2 < L) throw std::invalid_argument("slot rewritten before in-place use");
+          if (q.in1 == s) q.in1 = scratch;
+          if (!q.copy && q.in2 == s) q.in2 = scratch;
+        }
+    }
+    for (size_t r = 0; r < layers[L].size(); ++r) last_writer[layers[L][r].out] = {L, r};
+  }
+  p->TSdev = next_slot;
+  p->G.d = g.d;
+  p->G.S = (g.d + 1 + 3) / 4 * 4;
+  p->G.Q = p->Q;
+  p->G.slot_words = static_cast<int64_t>(p->Q) * p->G.S;
+  p->G.point_words = p->TSdev * p->G.slot_words;
+
+  cudaStream_t s = p->stream;
+  for (auto& rows : layers) {
+    if (rows.empty()) continue;
+    std::vector<int4> v;
+    v.reserve(rows.size());
+    for (auto& r : rows)
+      v.push_back(make_int4(static_cast<int>(r.in1), static_cast<int>(r.in2), static_cast<int>(r.out), r.copy));
+    int4* dv = dev_upload(v, s);
+    p->owned.push_back(dv);
+    p->conv_layers.emplace_back(dv, static_cast<int>(v.size()));
+  }
+  for (int32_t L = 0; L < g.n_add_layers; ++L) {
+    std::vector<int2> v;
+    for (int64_t t = g.add_layer_off[L]; t < g.add_layer_off[L + 1]; ++t)
+      v.push_back(make_int2(static_cast<int>(g.add_src[t]), static_cast<int>(g.add_dst[t])));
+    if (v.empty()) continue;
+    int2* dv = dev_upload(v, s);
+    p->owned.push_back(dv);
+    p->add_layers.emplace_back(dv, static_cast<int>(v.size()));
+  }
+  if (g.n_term_scales) {
+    std::vector<int2> v;
+    for (int64_t t = 0; t < g.n_term_scales; ++t) {
+      if (g.ts_factor[t] > (int64_t(1) << 30) || g.ts_factor[t] < -(int64_t(1) << 30))
+        throw std::invalid_argument("term scale factor out of range");
+      v.push_back(make_int2(static_cast<int>(g.ts_slot[t]), static_cast<int>(g.ts_factor[t])));
+    }
+    p->ts = dev_upload(v, s);
+    p->owned.push_back(p->ts);
+    p->nts = static_cast<int>(v.size());
+  }
+  std::vector<int> rs(g.n + 1), rm(g.n + 1, 1);
+  rs[0] = static_cast<int>(g.value_slot);
+  for (int i = 0; i < g.n; ++i) {
+    rs[1 + i] = g.gradient_slots[i] < 0 ? -1 : static_cast<int>(g.gradient_slots[i]);
+    if (g.multipliers[i] > (int64_t(1) << 30) || g.multipliers[i] < -(int64_t(1) << 30))
+      throw std::invalid_argument("multiplier out of range");
+    rm[1 + i] = static_cast<int>(g.multipliers[i]);
+  }
+  p->nrows = g.n + 1;
+  p->row_slot = dev_upload(rs, s);
+  p->row_mult = dev_upload(rm, s);
+  p->owned.push_back(p->row_slot);
+  p->owned.push_back(p->row_mult);
+
+  p->arena = dev_alloc<double>(static_cast<size_t>(max_batch) * p->G.point_words);
+  p->stage = dev_alloc<double>(static_cast<size_t>(p->Q) * max_batch * p->top * (g.d + 1));
+  p->vg = dev_alloc<double>(static_cast<size_t>(p->Q) * max_batch * p->nrows * (g.d + 1));
+  ck(cudaStreamSynchronize(s), "plan upload");
+
+  const Costs c = costs(g.m);
+  p->flops_model = flop_count(g, 0, c.rep_add, c.rep_mul);
+  p->alg_ops = alg_op_count(g);
+  p->conv_jobs = g.conv_layer_off[g.n_conv_layers];
+  p->add_jobs = g.add_layer_off[g.n_add_layers];
+  return p.release();
+}
+
+void fill_report(const Plan& p, int batch, pse_report* rep) {
+  rep->double_op_count = p.flops_model;
+  rep->alg_op_count = p.alg_ops;
+  rep->conv_jobs_executed = p.conv_jobs * batch;
+  rep->add_jobs_executed = p.add_jobs * batch;
+  rep->copy_jobs_executed = p.copy_jobs * batch;
+  rep->batch = batch;
+}
+
+void upload(Plan& p, int batch, const double* const* slabs, int64_t stride) {
+  if (batch < 1 || batch > p.max_batch) throw std::invalid_argument("batch outside [1, max_batch]");
+  if (!slabs) throw std::invalid_argument("null static slabs");
+  const int64_t pw = p.top * (p.d + 1);
+  if (stride == 0) stride = pw;
+  if (stride < pw) throw std::invalid_argument("point stride smaller than the static region");
+  ck(cudaSetDevice(p.device), "cudaSetDevice");
+  for (int q = 0; q < p.Q; ++q) {
+    if (!slabs[q]) throw std::invalid_argument("null static slab");
+    double* dst = p.stage + static_cast<int64_t>(q) * batch * pw;
+    if (stride == pw) {
+      ck(cudaMemcpyAsync(dst, slabs[q], sizeof(double) * batch * pw, cudaMemcpyHostToDevice, p.stream), "H2D");
+    } else {
+      ck(cudaMemcpy2DAsync(dst, pw * sizeof(double), slabs[q], stride * sizeof(double), pw * sizeof(double), batch,
+                           cudaMemcpyHostToDevice, p.stream),
+         "H2D");
+    }
+  }
+  const int64_t n = static_cast<int64_t>(p.Q) * batch * pw;
+  k_stage<<<grid_for(n, 256, p.sms), 256, 0, p.stream>>>(p.stage, p.arena, p.G, p.top, batch, pw);
+  ck(cudaGetLastError(), "stage launch");
+}
+
+int execute(Plan& p, int batch, int detail, pse_report* rep) {
+  if (batch < 1 || batch > p.max_batch) throw std::invalid_argument("batch outside [1, max_batch]");
+  ck(cudaSetDevice(p.device), "cudaSetDevice");
+  p.ensure_events(2);
+  int launches = 0;
+  if (detail) {
+    std::vector<std::pair<char, cudaEvent_t>> marks;
+    ck(cudaEventRecord(p.ev[0], p.stream), "event");
+    launches = p.launch_all(batch, &marks);
+    ck(cudaGetLastError(), "launch");
+    ck(cudaEventSynchronize(marks.back().second), "execute");
+    if (rep) {
+      double conv = 0, scale = 0, add = 0, wall = 0;
+      cudaEvent_t prev = p.ev[0];
+      for (auto& [kind, e] : marks) {
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, prev, e), "elapsed");
+        if (kind == 'c') conv += ms;
+        if (kind == 's') scale += ms;
+        if (kind == 'a') add += ms;
+        if (kind != 'e') wall += ms;
+        prev = e;
+      }
+      rep->conv_ms = conv;
+      rep->scale_ms = scale;
+      rep->add_ms = add;
+      rep->wall_ms = wall;
+    }
+  } else {
+    auto it = p.graphs.find(batch);
+    if (it == p.graphs.end()) {
+      cudaGraph_t graph;
+      ck(cudaStreamBeginCapture(p.stream, cudaStreamCaptureModeThreadLocal), "capture");
+      p.launch_all(batch, nullptr);
+      ck(cudaStreamEndCapture(p.stream, &graph), "capture end");
+      cudaGraphExec_t exec;
+      ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+      cudaGraphDestroy(graph);
+      it = p.graphs.emplace(batch, exec).first;
+    }
+    ck(cudaEventRecord(p.ev[0], p.stream), "event");
+    ck(cudaGraphLaunch(it->second, p.stream), "graph launch");
+    ck(cudaEventRecord(p.ev[1], p.stream), "event");
+    ck(cudaEventSynchronize(p.ev[1]), "execute");
+    launches = p.phase_count();
+    if (rep) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, p.ev[0], p.ev[1]), "elapsed");
+      rep->wall_ms = ms;
+      rep->conv_ms = rep->scale_ms = rep->add_ms = 0;
+    }
+  }
+  if (rep) {
+    fill_report(p, batch, rep);
+    rep->kernel_launches = launches;
+  }
+  return PSE_OK;
+}
+
+void download(Plan& p, int batch, double* const* vg_out, double* const* dyn_out) {
+  if (batch < 1 || batch > p.max_batch) throw std::invalid_argument("batch outside [1, max_batch]");
+  ck(cudaSetDevice(p.device), "cudaSetDevice");
+  const int64_t vw = static_cast<int64_t>(batch) * p.nrows * (p.d + 1);
+  if (vg_out)
+    for (int q = 0; q < p.Q; ++q)
+      ck(cudaMemcpyAsync(vg_out[q], p.vg + static_cast<int64_t>(q) * vw, vw * sizeof(double),
+                         cudaMemcpyDeviceToHost, p.stream),
+         "D2H");
+  if (dyn_out) {
+    const int64_t dw = static_cast<int64_t>(batch) * p.TS * (p.d + 1);
+    if (!p.dyn) p.dyn = dev_alloc<double>(static_cast<size_t>(p.Q) * p.max_batch * p.TS * (p.d + 1));
+    const int64_t n = static_cast<int64_t>(p.Q) * dw;
+    k_export<<<grid_for(n, 256, p.sms), 256, 0, p.stream>>>(p.arena, p.dyn, p.G, p.TS, batch);
+    ck(cudaGetLastError(), "export launch");
+    for (int q = 0; q < p.Q; ++q)
+      ck(cudaMemcpyAsync(dyn_out[q], p.dyn + static_cast<int64_t>(q) * dw, dw * sizeof(double),
+                         cudaMemcpyDeviceToHost, p.stream),
+         "D2H");
+  }
+  ck(cudaStreamSynchronize(p.stream), "download");
+}
+
+// fold_exponents (jobgraph.cpp:168-197) as prologue conv jobs: for each
+// monomial with exponents, folded = a_k; for each position j with e_j > 1:
+// power = z (then power = conv(power, z), e_j - 2 times); folded =
+// conv(folded, power). The final folded series is copied into a_k's slot,
+// exactly where the reference stages it.
+std::vector<std::vector<ConvRow>> fold_prologue(const HostGraph& hg, int64_t first_scratch, int64_t* nslots) {
+  std::vector<std::vector<ConvRow>> layers;
+  int64_t next = first_scratch;
+  auto put = [&](size_t layer, ConvRow r) {
+    if (layers.size() <= layer) layers.resize(layer + 1);
+    layers[layer].push_back(r);
+  };
+  for (int k = 0; k < hg.N; ++k) {
+    if (!hg.has_exponents(k)) continue;
+    int64_t folded = 1 + k;
+    size_t ready = 0;  // first layer at which `folded` is readable
+    bool any = false;
+    for (int64_t p = hg.mono_start[k]; p < hg.mono_start[k + 1]; ++p) {
+      const int e = hg.exponents[p];
+      if (e <= 1) continue;
+      const int64_t z = hg.N + hg.indices[p];
+      int64_t power = z;
+      size_t pready = 0;
+      for (int q = 2; q <= e - 1; ++q) {
+        const int64_t out = next++;
+        put(pready, {power, z, out, 0});
+        power = out;
+        ++pready;
+      }
+      const int64_t out = next++;
+      const size_t L = std::max(ready, pready);
+      put(L, {folded, power, out, 0});
+      folded = out;
+      ready = L + 1;
+      any = true;
+    }
+    if (any) put(ready, {folded, 0, 1 + k, 1});
+  }
+  *nslots = next - first_scratch;
+  return layers;
+}
+
+}  // namespace
+}  // namespace pse
+
+struct pse_plan {
+  std::unique_ptr<pse::Plan> p;
+};
+
+extern "C" {
+
+int pse_plan_create(const pse_graph_desc* desc, int32_t device, int32_t max_batch, pse_plan** out) {
+  return pse::guarded([&] {
+    if (!desc || !out) throw std::invalid_argument("null argument");
+    auto* h = new pse_plan;
+    h->p.reset(pse::build_plan(*desc, device, max_batch, {}, 0));
+    *out = h;
+    return PSE_OK;
+  });
+}
+
+void pse_plan_destroy(pse_plan* p) { delete p; }
+
+int pse_plan_upload(pse_plan* p, int32_t batch, const double* const* static_slabs, int64_t point_stride) {
+  return pse::guarded([&] {
+    if (!p) throw std::invalid_argument("null plan");
+    pse::upload(*p->p, batch, static_slabs, point_stride);
+    pse::ck(cudaStreamSynchronize(p->p->stream), "upload");
+    return PSE_OK;
+  });
+}
+
+int pse_plan_execute(pse_plan* p, int32_t batch, int32_t detail, pse_report* rep) {
+  return pse::guarded([&] {
+    if (!p) throw std::invalid_argument("null plan");
+    if (rep) std::memset(rep, 0, sizeof *rep);
+    return pse::execute(*p->p, batch, detail, rep);
+  });
+}
+
+int pse_plan_download(pse_plan* p, int32_t batch, double* const* value_grad_out, double* const* dyn_slabs_out) {
+  return pse::guarded([&] {
+    if (!p) throw std::invalid_argument("null plan");
+    pse::download(*p->p, batch, value_grad_out, dyn_slabs_out);
+    return PSE_OK;
+  });
+}
+
+int pse_plan_run(pse_plan* p, int32_t batch, const double* const* static_slabs, int64_t point_stride,
+                 double* const* dyn_slabs_out, double* const* value_grad_out, pse_report* rep) {
+  return pse::guarded([&] {
+    if (!p) throw std::invalid_argument("null plan");
+    pse::Plan& P = *p->p;
+    pse::ck(cudaSetDevice(P.device), "cudaSetDevice");
+    cudaEvent_t e0, e1, e2, e3;
+    pse::ck(cudaEventCreate(&e0), "event");
+    pse::ck(cudaEventCreate(&e1), "event");
+    pse::ck(cudaEventCreate(&e2), "event");
+    pse::ck(cudaEventCreate(&e3), "event");
+    pse::ck(cudaEventRecord(e0, P.stream), "event");
+    pse::upload(P, batch, static_slabs, point_stride);
+    pse::ck(cudaEventRecord(e1, P.stream), "event");
+    pse_report r{};
+    pse::execute(P, batch, 0, &r);
+    pse::ck(cudaEventRecord(e2, P.stream), "event");
+    pse::download(P, batch, value_grad_out, dyn_slabs_out);
+    pse::ck(cudaEventRecord(e3, P.stream), "event");
+    pse::ck(cudaEventSynchronize(e3), "run");
+    float h2d = 0, d2h = 0, all = 0;
+    cudaEventElapsedTime(&h2d, e0, e1);
+    cudaEventElapsedTime(&d2h, e2, e3);
+    cudaEventElapsedTime(&all, e0, e3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaEventDestroy(e2);
+    cudaEventDestroy(e3);
+    r.h2d_ms = h2d;
+    r.d2h_ms = d2h;
+    r.e2e_ms = all;
+    r.kernel_launches += 1 + (dyn_slabs_out ? 1 : 0);
+    if (rep) *rep = r;
+    return PSE_OK;
+  });
+}
+
+int pse_plan_info(const pse_plan* p, int64_t* out) {
+  if (!p || !out) return PSE_EINVAL;
+  const pse::Plan& P = *p->p;
+  int64_t v[8] = {P.n, P.N, P.d, P.m, P.mode, P.TS, P.top, P.max_batch};
+  std::memcpy(out, v, sizeof v);
+  return PSE_OK;
+}
+
+int pse_evaluate(int32_t n, int32_t d, int32_t m, int32_t mode, int32_t N, const int32_t* nvars,
+                 const int32_t* indices, const int32_t* exponents, int32_t batch, const double* stat,
+                 double* vg_out, int32_t device, pse_report* rep) {
+  return pse::guarded([&] {
+    if (!nvars || !indices || !stat || !vg_out) throw std::invalid_argument("null argument");
+    if (!pse::valid_precision(m)) throw std::invalid_argument("unsupported precision level");
+    if (batch < 1) throw std::invalid_argument("batch must be at least 1");
+    pse::HostGraph hg = pse::build_graph(n, d, N, nvars, indices, exponents);
+    const pse_graph_desc desc = pse::describe(hg, m, mode);
+    int64_t extra = 0;
+    auto pro = pse::fold_prologue(hg, hg.total_slots, &extra);
+    std::unique_ptr<pse::Plan> P(pse::build_plan(desc, device, batch, pro, extra));
+    const int Q = P->Q;
+    const int64_t pw = P->top * (d + 1);
+    std::vector<const double*> slabs(Q);
+    for (int q = 0; q < Q; ++q) slabs[q] = stat + static_cast<int64_t>(q) * batch * pw;
+    const int64_t vw = static_cast<int64_t>(batch) * (n + 1) * (d + 1);
+    std::vector<double*> outs(Q);
+    for (int q = 0; q < Q; ++q) outs[q] = vg_out + q * vw;
+    pse::upload(*P, batch, slabs.data(), pw);
+    pse_report r{};
+    pse::execute(*P, batch, 1, &r);
+    pse::download(*P, batch, outs.data(), nullptr);
+    if (rep) *rep = r;
+    return PSE_OK;
+  });
+}
+
+int pse_md_apply(int32_t op, int32_t m, int32_t impl, int64_t count, const double* x, const double* y, double* out,
+                 int32_t device) {
+  return pse::guarded([&] {
+    if (!pse::valid_precision(m)) throw std::invalid_argument("unsupported precision level");
+    if (op < 0 || op > 2 || count < 0) throw std::invalid_argument("bad md op");
+    if (count == 0) return PSE_OK;
+    pse::ck(cudaSetDevice(device), "cudaSetDevice");
+    const size_t bytes = static_cast<size_t>(count) * m * sizeof(double);
+    double *dx, *dy, *dz;
+    pse::ck(cudaMalloc(&dx, bytes), "cudaMalloc");
+    pse::ck(cudaMalloc(&dy, bytes), "cudaMalloc");
+    pse::ck(cudaMalloc(&dz, bytes), "cudaMalloc");
+    pse::ck(cudaMemcpy(dx, x, bytes, cudaMemcpyHostToDevice), "H2D");
+    pse::ck(cudaMemcpy(dy, y, bytes, cudaMemcpyHostToDevice), "H2D");
+    pse::MdArgs a{op, impl, count, dx, dy, dz};
+    const pse::Launchers* L = pse::launchers_for(m, false);
+    L->prepare();
+    L->md(a, nullptr);
+    pse::ck(cudaGetLastError(), "md launch");
+    pse::ck(cudaMemcpy(out, dz, bytes, cudaMemcpyDeviceToHost), "D2H");
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(dz);
+    return PSE_OK;
+  });
+}
+
+int pse_series_conv(int32_t d, int32_t m, int32_t mode, int64_t count, const double* x, const double* y, double* z,
+                    int32_t device) {
+  return pse::guarded([&] {
+    if (!pse::valid_precision(m) || d < 0 || count < 0) throw std::invalid_argument("bad series arguments");
+    if (count == 0) return PSE_OK;
+    pse::ck(cudaSetDevice(device), "cudaSetDevice");
+    const int Q = (mode == PSE_MODE_COMPLEX ? 2 : 1) * m;
+    pse::Geom G;
+    G.d = d;
+    G.S = d + 1;
+    G.Q = Q;
+    G.slot_words = static_cast<int64_t>(Q) * G.S;
+    G.point_words = 3 * G.slot_words;  // slots x, y, z per pair
+    const size_t words = static_cast<size_t>(count) * G.point_words;
+    double* arena;
+    pse::ck(cudaMalloc(&arena, words * sizeof(double)), "cudaMalloc");
+    const int64_t sw = G.slot_words;
+    pse::ck(cudaMemcpy2D(arena, 3 * sw * sizeof(double), x, sw * sizeof(double), sw * sizeof(double), count,
+                         cudaMemcpyHostToDevice),
+            "H2D");
+    pse::ck(cudaMemcpy2D(arena + sw, 3 * sw * sizeof(double), y, sw * sizeof(double), sw * sizeof(double), count,
+                         cudaMemcpyHostToDevice),
+            "H2D");
+    int4* job;
+    pse::ck(cudaMalloc(&job, sizeof(int4)), "cudaMalloc");
+    const int4 hj = make_int4(0, 1, 2, 0);
+    pse::ck(cudaMemcpy(job, &hj, sizeof hj, cudaMemcpyHostToDevice), "H2D");
+    pse::ConvArgs a{arena, G, job, 1, (d + 2) / 2, static_cast<int>(count)};
+    const pse::Launchers* L = pse::launchers_for(m, mode == PSE_MODE_COMPLEX);
+    L->prepare();
+    L->conv(a, nullptr);
+    pse::ck(cudaGetLastError(), "conv launch");
+    pse::ck(cudaMemcpy2D(z, sw * sizeof(double), arena + 2 * sw, 3 * sw * sizeof(double), sw * sizeof(double), count,
+                         cudaMemcpyDeviceToHost),
+            "D2H");
+    cudaFree(job);
+    cudaFree(arena);
+    return PSE_OK;
+  });
+}
+
+void* pse_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+    pse::set_error("cudaHostAlloc failed");
+    return nullptr;
+  }
+  return p;
+}
+
+void pse_host_free(void* p) { cudaFreeHost(p); }
+
+int pse_device_info(int32_t device, int64_t* out) {
+  return pse::guarded([&] {
+    int count = 0;
+    pse::ck(cudaGetDeviceCount(&count), "device count");
+    cudaDeviceProp prop;
+    pse::ck(cudaGetDeviceProperties(&prop, device), "props");
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, device);
+    out[0] = prop.multiProcessorCount;
+    out[1] = clk;
+    out[2] = prop.major * 10 + prop.minor;
+    out[3] = count;
+    return PSE_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,414 @@
+// Device kernels of the evaluate-and-differentiate engine, templated on the
+// limb count M (1,2,3,4,5,8,10) and complex mode. Instantiated once per M in
+// kernels_m<M>.cu so the heavy M=8/10 bodies compile in parallel.
+//
+// Arena layout in HBM (one per evaluation point):
+//   arena[point][slot][q][S],  q = part*M + limb, S = (d+1) rounded up to 4
+// i.e. a slot's series is one contiguous, limb-split structure of arrays:
+// lanes that own consecutive coefficients load consecutive doubles of the
+// same limb (coalesced), and a whole slot is a single 32B-aligned span.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "md.cuh"
+
+namespace pse {
+
+struct Geom {
+  int d;              // truncation degree
+  int S;              // padded coefficient stride
+  int Q;              // slabs per slot (P * M)
+  int64_t slot_words; // Q * S
+  int64_t point_words;// device slots * Q * S
+};
+
+struct ConvArgs {
+  double* arena;
+  Geom G;
+  const int4* jobs;  // (in1, in2, out, copy) of one conv layer
+  int njobs;
+  int npairs;        // coefficient pairs per job: (d+2)/2
+  int batch;
+};
+
+struct AddArgs {
+  double* arena;
+  Geom G;
+  const int2* jobs;  // (src, dst): dst := dst + src
+  int njobs;
+  int batch;
+};
+
+struct ScaleArgs {
+  double* arena;
+  Geom G;
+  const int2* items;  // (slot, factor) -- factors are small exact integers
+  int nitems;
+  int batch;
+};
+
+struct ExtractArgs {
+  const double* arena;
+  Geom G;
+  const int* row_slot;   // [nrows] slot or -1 (zero series)
+  const int* row_mult;   // [nrows] integer multiplier
+  int nrows;
+  int batch;
+  double* out;           // [Q][batch][nrows][d+1]
+};
+
+struct MdArgs {
+  int op;    // 0 add, 1 sub, 2 mul
+  int impl;  // 0 fast (engine path), 1 literal
+  int64_t count;
+  const double* x;  // [count][M]
+  const double* y;
+  double* out;
+};
+
+struct Launchers {
+  void (*conv)(const ConvArgs&, cudaStream_t);
+  void (*add)(const AddArgs&, cudaStream_t);
+  void (*scale)(const ScaleArgs&, cudaStream_t);
+  void (*extract)(const ExtractArgs&, cudaStream_t);
+  void (*md)(const MdArgs&, cudaStream_t);
+  void (*prepare)();  // sets kernel attributes on the current device
+  int lane_words;
+};
+
+#ifdef PSE_KERNELS_IMPL
+
+constexpr int kConvThreads = 128;
+constexpr int kAddThreads = 128;
+
+template <int M>
+__device__ __forceinline__ void load_md(const double* __restrict__ src, int S, int j, double (&v)[M]) {
+#pragma unroll
+  for (int q = 0; q < M; ++q) v[q] = src[q * S + j];
+}
+
+template <int M>
+__device__ __forceinline__ void store_md(double* dst, int S, int j, const double (&v)[M]) {
+#pragma unroll
+  for (int q = 0; q < M; ++q) dst[q * S + j] = v[q];
+}
+
+template <int M>
+__device__ __forceinline__ void copy_md(double (&d)[M], const double (&s)[M]) {
+#pragma unroll
+  for (int q = 0; q < M; ++q) d[q] = s[q];
+}
+
+// ------------------------------------------------------------- convolution
+// One thread per (point, job, coefficient pair). Pair p owns output
+// coefficients k1 = p and k2 = d - p, so every thread performs d+2 products
+// (when d is even the middle pair k1 = k2 = d/2 performs d/2+1) and warps
+// stay load-balanced. Each z_k is accumulated by one thread in ascending i
+// exactly as conv() does (pseries.cpp:41-48): acc = x0*y_k, then
+// acc = md_add(acc, x_i*y_{k-i}) -- the bit-exactness contract.
+// Consecutive lanes are consecutive pairs of one job: x_i is a broadcast
+// load and y_{k-i} a coalesced one.
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kConvThreads) k_conv(const ConvArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * a.npairs;
+  if (g >= ntasks) return;
+  const int pair = static_cast<int>(g % a.npairs);
+  const int64_t r = g / a.npairs;
+  const int jb = static_cast<int>(r % a.njobs);
+  const int64_t pt = r / a.njobs;
+  const int4 J = a.jobs[jb];
+  const int S = a.G.S, d = a.G.d;
+  double* base = a.arena + pt * a.G.point_words;
+  const double* __restrict__ X = base + static_cast<int64_t>(J.x) * a.G.slot_words;
+  const double* __restrict__ Y = base + static_cast<int64_t>(J.y) * a.G.slot_words;
+  double* Z = base + static_cast<int64_t>(J.z) * a.G.slot_words;
+  const int k1 = pair, k2 = d - pair;
+  constexpr int Q = CPLX ? 2 * M : M;
+
+  if (J.w) {  // copy job (executor.cpp:130-133): out := in1
+#pragma unroll 1
+    for (int q = 0; q < Q; ++q) {
+      Z[q * S + k1] = X[q * S + k1];
+      if (k2 != k1) Z[q * S + k2] = X[q * S + k2];
+    }
+    return;
+  }
+
+  const int n1 = k1 + 1;
+  const int total = k2 > k1 ? d + 2 : n1;
+  double ar[M], ai[M];   // accumulators (re, im)
+  double xr[M], yr[M];   // current operands (re)
+  double xi[M], yi[M];   // current operands (im, complex only)
+  load_md<M>(X, S, 0, xr);
+  load_md<M>(Y, S, k1, yr);
+  if constexpr (CPLX) {
+    load_md<M>(X + M * S, S, 0, xi);
+    load_md<M>(Y + M * S, S, k1, yi);
+  }
+#pragma unroll 1
+  for (int t = 0; t < total; ++t) {
+    const bool second = t >= n1;
+    const int kk = second ? k2 : k1;
+    const int i = second ? t - n1 : t;
+    // next operands: (kk, i+1) or the start of the second chain
+    const int tn = t + 1;
+    const bool nsecond = tn >= n1;
+    const int ni = nsecond ? tn - n1 : tn;
+    const int nk = nsecond ? k2 : k1;
+    const bool more = tn < total;
+    if constexpr (!CPLX) {
+      double p[M];
+      exp_mul_fast<M>(xr, yr, p, sm);
+      if (more) {
+        load_md<M>(X, S, ni, xr);
+        load_md<M>(Y, S, nk - ni, yr);
+      }
+      if (i == 0)
+        copy_md<M>(ar, p);
+      else
+        exp_add_fast<M>(ar, p, ar, sm);
+    } else {
+      // (xr + i xi)(yr + i yi): pseries.cpp:50-51 operand order
+      double p1[M], p2[M], pre[M], pim[M];
+      exp_mul_fast<M>(xr, yr, p1, sm);
+      exp_mul_fast<M>(xi, yi, p2, sm);
+      exp_sub_fast<M>(p1, p2, pre, sm);
+      exp_mul_fast<M>(xr, yi, p1, sm);
+      exp_mul_fast<M>(xi, yr, p2, sm);
+      exp_add_fast<M>(p1, p2, pim, sm);
+      if (more) {
+        load_md<M>(X, S, ni, xr);
+        load_md<M>(Y, S, nk - ni, yr);
+        load_md<M>(X + M * S, S, ni, xi);
+        load_md<M>(Y + M * S, S, nk - ni, yi);
+      }
+      if (i == 0) {
+        copy_md<M>(ar, pre);
+        copy_md<M>(ai, pim);
+      } else {
+        exp_add_fast<M>(ar, pre, ar, sm);
+        exp_add_fast<M>(ai, pim, ai, sm);
+      }
+    }
+    if (i == kk) {
+      store_md<M>(Z, S, kk, ar);
+      if constexpr (CPLX) store_md<M>(Z + M * S, S, kk, ai);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- addition
+// One thread per (point, job, coefficient): dst_k := md_add(dst_k, src_k)
+// (executor.cpp:144-148, operand order x = dst, y = src).
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kAddThreads) k_add(const AddArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const int d1 = a.G.d + 1;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * d1;
+  if (g >= ntasks) return;
+  const int k = static_cast<int>(g % d1);
+  const int64_t r = g / d1;
+  const int jb = static_cast<int>(r % a.njobs);
+  const int64_t pt = r / a.njobs;
+  const int2 J = a.jobs[jb];
+  const int S = a.G.S;
+  double* base = a.arena + pt * a.G.point_words;
+  const double* src = base + static_cast<int64_t>(J.x) * a.G.slot_words;
+  double* dst = base + static_cast<int64_t>(J.y) * a.G.slot_words;
+#pragma unroll
+  for (int part = 0; part < (CPLX ? 2 : 1); ++part) {
+    double x[M], y[M], z[M];
+    load_md<M>(dst + part * M * S, S, k, x);
+    load_md<M>(src + part * M * S, S, k, y);
+    exp_add_fast<M>(x, y, z, sm);
+    store_md<M>(dst + part * M * S, S, k, z);
+  }
+}
+
+// ------------------------------------------------------------ scale phase
+// TermScale (executor.cpp:138-143 -> series_scale_int, pseries.cpp:85-93)
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kAddThreads) k_scale(const ScaleArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const int d1 = a.G.d + 1;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.nitems * d1;
+  if (g >= ntasks) return;
+  const int k = static_cast<int>(g % d1);
+  const int64_t r = g / d1;
+  const int it = static_cast<int>(r % a.nitems);
+  const int64_t pt = r / a.nitems;
+  const int2 T = a.items[it];
+  const int S = a.G.S;
+  double* s = a.arena + pt * a.G.point_words + static_cast<int64_t>(T.x) * a.G.slot_words;
+  double c[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) c[q] = q == 0 ? static_cast<double>(T.y) : 0.0;
+#pragma unroll
+  for (int part = 0; part < (CPLX ? 2 : 1); ++part) {
+    double x[M], z[M];
+    load_md<M>(s + part * M * S, S, k, x);
+    exp_mul_fast<M>(x, c, z, sm);
+    store_md<M>(s + part * M * S, S, k, z);
+  }
+}
+
+// ----------------------------------------------------------------- extract
+// extract (executor.cpp:254-269): value row then one row per variable,
+// multiplier applied with md_mul, absent variables give zero series.
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kAddThreads) k_extract(const ExtractArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const int d1 = a.G.d + 1;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.nrows * d1;
+  if (g >= ntasks) return;
+  const int k = static_cast<int>(g % d1);
+  const int64_t r = g / d1;
+  const int row = static_cast<int>(r % a.nrows);
+  const int64_t pt = r / a.nrows;
+  const int slot = a.row_slot[row];
+  const int mult = a.row_mult[row];
+  const int S = a.G.S;
+  const int64_t plane = static_cast<int64_t>(a.batch) * a.nrows * d1;  // words per q
+  double* out = a.out + (pt * a.nrows + row) * d1 + k;
+#pragma unroll
+  for (int part = 0; part < (CPLX ? 2 : 1); ++part) {
+    double x[M];
+    if (slot < 0) {
+#pragma unroll
+      for (int q = 0; q < M; ++q) x[q] = 0.0;
+    } else {
+      const double* s = a.arena + pt * a.G.point_words + static_cast<int64_t>(slot) * a.G.slot_words;
+      load_md<M>(s + part * M * S, S, k, x);
+      if (mult != 1) {
+        double c[M], z[M];
+#pragma unroll
+        for (int q = 0; q < M; ++q) c[q] = q == 0 ? static_cast<double>(mult) : 0.0;
+        exp_mul_fast<M>(x, c, z, sm);
+        copy_md<M>(x, z);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < M; ++q) out[(part * M + q) * plane] = x[q];
+  }
+}
+
+// --------------------------------------------------------- md primitives
+template <int M>
+__global__ void __launch_bounds__(kAddThreads) k_md(const MdArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= a.count) return;
+  double x[M], y[M], z[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    x[q] = a.x[c * M + q];
+    y[q] = a.y[c * M + q];
+  }
+  if (a.impl == 1) {
+    double ny[M];
+    if (a.op == 1) {
+#pragma unroll
+      for (int q = 0; q < M; ++q) ny[q] = -y[q];
+    }
+    if (a.op == 0) exp_add_lit<M>(x, y, z);
+    else if (a.op == 1) {
+      if constexpr (M == 1) z[0] = __dsub_rn(x[0], y[0]);
+      else exp_add_lit<M>(x, ny, z);
+    } else exp_mul_lit<M>(x, y, z);
+  } else {
+    if (a.op == 0) exp_add_fast<M>(x, y, z, sm);
+    else if (a.op == 1) exp_sub_fast<M>(x, y, z, sm);
+    else exp_mul_fast<M>(x, y, z, sm);
+  }
+#pragma unroll
+  for (int q = 0; q < M; ++q) a.out[c * M + q] = z[q];
+}
+
+template <int M, bool CPLX>
+struct Impl {
+  static size_t smem(int threads) { return static_cast<size_t>(threads) * MdTraits<M>::LANE * sizeof(double); }
+  static void conv(const ConvArgs& a, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(a.batch) * a.njobs * a.npairs;
+    if (n == 0) return;
+    const size_t sh = smem(kConvThreads);
+    k_conv<M, CPLX><<<static_cast<unsigned>((n + kConvThreads - 1) / kConvThreads), kConvThreads, sh, s>>>(a);
+  }
+  static void add(const AddArgs& a, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(a.batch) * a.njobs * (a.G.d + 1);
+    if (n == 0) return;
+    const size_t sh = smem(kAddThreads);
+    k_add<M, CPLX><<<static_cast<unsigned>((n + kAddThreads - 1) / kAddThreads), kAddThreads, sh, s>>>(a);
+  }
+  static void scale(const ScaleArgs& a, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(a.batch) * a.nitems * (a.G.d + 1);
+    if (n == 0) return;
+    const size_t sh = smem(kAddThreads);
+    k_scale<M, CPLX><<<static_cast<unsigned>((n + kAddThreads - 1) / kAddThreads), kAddThreads, sh, s>>>(a);
+  }
+  static void extract(const ExtractArgs& a, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(a.batch) * a.nrows * (a.G.d + 1);
+    if (n == 0) return;
+    const size_t sh = smem(kAddThreads);
+    k_extract<M, CPLX><<<static_cast<unsigned>((n + kAddThreads - 1) / kAddThreads), kAddThreads, sh, s>>>(a);
+  }
+  static void md(const MdArgs& a, cudaStream_t s) {
+    if (a.count == 0) return;
+    const size_t sh = smem(kAddThreads);
+    k_md<M><<<static_cast<unsigned>((a.count + kAddThreads - 1) / kAddThreads), kAddThreads, sh, s>>>(a);
+  }
+  static void prepare() {
+    const int c = static_cast<int>(smem(kConvThreads)), o = static_cast<int>(smem(kAddThreads));
+    cudaFuncSetAttribute(k_conv<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
+    cudaFuncSetAttribute(k_add<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
+    cudaFuncSetAttribute(k_scale<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
+    cudaFuncSetAttribute(k_extract<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
+    cudaFuncSetAttribute(k_md<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
+  }
+  static const Launchers* table() {
+    static const Launchers L{&conv, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE};
+    return &L;
+  }
+};
+
+#define PSE_INSTANTIATE(M)                                                              \
+  const Launchers* launchers_m##M(bool cplx) {                                           \
+    return cplx ? Impl<M, true>::table() : Impl<M, false>::table();                      \
+  }
+
+#endif  // PSE_KERNELS_IMPL
+
+const Launchers* launchers_m1(bool);
+const Launchers* launchers_m2(bool);
+const Launchers* launchers_m3(bool);
+const Launchers* launchers_m4(bool);
+const Launchers* launchers_m5(bool);
+const Launchers* launchers_m8(bool);
+const Launchers* launchers_m10(bool);
+
+inline const Launchers* launchers_for(int m, bool cplx) {
+  switch (m) {
+    case 1: return launchers_m1(cplx);
+    case 2: return launchers_m2(cplx);
+    case 3: return launchers_m3(cplx);
+    case 4: return launchers_m4(cplx);
+    case 5: return launchers_m5(cplx);
+    case 8: return launchers_m8(cplx);
+    case 10: return launchers_m10(cplx);
+    default: return nullptr;
+  }
+}
+
+}  // namespace pse

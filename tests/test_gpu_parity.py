@@ -1,0 +1,188 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the CPU oracle,
+bit for bit. Mirrors the reference's own assertions:
+  engine == eval_direct on positive-integer instances  (test_executor.cpp:148-179)
+  device == run_sequential on p1, d in {8,31}, m in {1,2,4} (acceptance.cpp:163-189)
+  md identities bitwise (test_multidouble.cpp:148-163)
+plus bitwise equality with the oracle on full-precision instances for every
+precision level, on the C1 correctness configuration, and through the
+batched multi-point path."""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from instances import assert_bitwise, int_instance, md_instance
+
+pe = pytest.importorskip("paper_2101_10881_b200")
+
+pytestmark = pytest.mark.gpu
+LEVELS = [1, 2, 3, 4, 5, 8, 10]
+
+
+def dev_eval(p: po.Problem, batch_stat=None):
+    """evaluate() on the device for one problem; returns vg [P][m][n+1][d+1]."""
+    Q = p.P * p.m
+    st = p.stat.reshape(Q, 1, *p.stat.shape[2:]) if batch_stat is None else batch_stat
+    vg, rep = pe.evaluate_packed(p.n, p.d, p.m, "cplx" if p.cplx else "real", p.nvars, p.idx, p.exps, st,
+                                 st.shape[1])
+    return vg, rep
+
+
+# ---------------------------------------------------------------- md ops
+@pytest.mark.parametrize("m", LEVELS)
+@pytest.mark.parametrize("impl", ["fast", "lit"])
+def test_md_ops_bitwise_random(m, impl):
+    x = po.random_md(1000 + m, m, 200_000)
+    y = po.random_md(2000 + m, m, 200_000)
+    for op in ("add", "sub", "mul"):
+        assert_bitwise(pe.md_apply(op, x, y, impl), po.md_op(op, x, y), f"{op} m={m} {impl}")
+
+
+@pytest.mark.parametrize("m", LEVELS)
+def test_md_ops_bitwise_edge_cases(m):
+    rng = np.random.default_rng(m)
+    base = po.random_md(77 + m, m, 64)
+    specials = []
+    z = np.zeros(m)
+    nz = -np.zeros(m)
+    one = np.zeros(m)
+    one[0] = 1.0
+    specials += [z, nz, one, -one]
+    for v in base[:16]:
+        specials += [v, -v]
+        w = v.copy()
+        w[1:] = 0.0
+        specials.append(w)  # leading limb only
+        if m > 1:
+            u = v.copy()
+            u[-1] = -0.0
+            specials.append(u)
+    ints = np.zeros((32, m))
+    ints[:, 0] = rng.integers(-50, 50, 32)
+    specials += list(ints)
+    S = np.array(specials)
+    X = np.repeat(S, len(S), 0)
+    Y = np.tile(S, (len(S), 1))
+    for op in ("add", "sub", "mul"):
+        assert_bitwise(pe.md_apply(op, X, Y, "fast"), po.md_op(op, X, Y), f"{op} m={m} edge")
+
+
+@pytest.mark.parametrize("m", LEVELS)
+def test_md_identities(m):
+    """x+0, x-0, x*1 bitwise x; x*0 all zeros (test_multidouble.cpp:148-163)."""
+    x = po.random_md(4000 + m, m, 300)
+    zero = np.zeros_like(x)
+    one = np.zeros_like(x)
+    one[:, 0] = 1.0
+    assert_bitwise(pe.md_apply("add", x, zero), x, "x+0")
+    assert_bitwise(pe.md_apply("sub", x, zero), x, "x-0")
+    assert_bitwise(pe.md_apply("mul", x, one), x, "x*1")
+    assert (pe.md_apply("mul", x, zero) == 0.0).all()
+
+
+# ---------------------------------------------------------------- series conv
+@pytest.mark.parametrize("m", LEVELS)
+@pytest.mark.parametrize("cplx", [False, True])
+def test_series_conv_bitwise(m, cplx):
+    rng = np.random.default_rng(10 * m + cplx)
+    P = 2 if cplx else 1
+    for d in (0, 1, 2, 7, 16, 33):
+        cnt = 5
+        x = po.random_md(int(rng.integers(1, 2**60)), m, cnt * P * (d + 1)).reshape(cnt, P, d + 1, m).transpose(0, 1, 3, 2).copy()
+        y = po.random_md(int(rng.integers(1, 2**60)), m, cnt * P * (d + 1)).reshape(cnt, P, d + 1, m).transpose(0, 1, 3, 2).copy()
+        z = pe.series_conv(x, y, "cplx" if cplx else "real")
+        for c in range(cnt):
+            assert_bitwise(z[c], po.series_conv(x[c], y[c], cplx), f"conv d={d} m={m} c={c}")
+
+
+# ---------------------------------------------------------------- whole engine
+def test_c1_bitwise_vs_reference_engine():
+    """C1: p1, d=15, m=2, seed 7 -- value, all 16 gradients and the whole
+    dynamic arena equal run_sequential bit for bit."""
+    p = po.gen_benchmark("p1", 15, 2, seed=7)
+    ref_vg, ref_dyn = po.evaluate(p, "ref" if po.has_ref() else "port", want_dyn=True)
+    pr = pe.gen_benchmark("p1", 15, 2, seed=7)
+    g = pe.build_jobgraph_shape(pr.n, pr.d, pr.nvars, pr.indices)
+    plan = pe.DevicePlan(g, 2, "real", 0, 1)
+    vg, dyn, rep = plan.run(pr.stat, 1, want_dyn=True)
+    assert_bitwise(vg[:, 0], ref_vg.reshape(2, 17, 16), "C1 value/gradients")
+    assert_bitwise(dyn[:, 0], ref_dyn.reshape(2, -1, 16), "C1 arena")
+    assert rep.conv_jobs_executed == 16380 and rep.add_jobs_executed == 9084
+    assert rep.double_op_count == po.flop_count(p, 39, 94)
+
+
+@pytest.mark.parametrize("d", [8, 31])
+@pytest.mark.parametrize("m", [1, 2, 4])
+def test_p1_bitwise_vs_sequential(d, m):
+    """acceptance criterion 6 (acceptance.cpp:163-189) with the device engine."""
+    p = po.gen_benchmark("p1", d, m, seed=7)
+    ref = po.evaluate(p, "port")
+    vg, _ = dev_eval(p)
+    assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"p1 d={d} m={m}")
+
+
+@pytest.mark.parametrize("pid,d,m", [("p2", 3, 2), ("p3", 3, 2), ("p2", 8, 10), ("p3", 2, 10)])
+def test_p2_p3_bitwise(pid, d, m):
+    p = po.gen_benchmark(pid, d, m, seed=7)
+    ref = po.evaluate(p, "port")
+    vg, _ = dev_eval(p)
+    assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"{pid} d={d} m={m}")
+
+
+def test_integer_instances_equal_direct_oracle():
+    """200 positive-integer instances (half with exponents): device ==
+    eval_direct bitwise (test_executor.cpp:148-159, acceptance criterion 5)."""
+    rng = np.random.default_rng(506)
+    for it in range(200):
+        p = int_instance(rng, it % 2 == 1)
+        ref = po.eval_direct(p)
+        vg, _ = dev_eval(p)
+        assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"int instance {it}")
+
+
+def test_complex_integer_instances_equal_direct_oracle():
+    rng = np.random.default_rng(507)
+    for it in range(40):
+        p = int_instance(rng, False, cplx=True)
+        ref = po.eval_direct(p)
+        vg, _ = dev_eval(p)
+        assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"complex int instance {it}")
+
+
+@pytest.mark.parametrize("m", LEVELS)
+@pytest.mark.parametrize("cplx", [False, True])
+def test_md_instances_bitwise_vs_oracle(m, cplx):
+    rng = np.random.default_rng(900 + m + 50 * cplx)
+    for it in range(12):
+        p = md_instance(rng, m, cplx, with_exponents=it % 3 == 0)
+        ref = po.evaluate(p, "port")
+        vg, _ = dev_eval(p)
+        assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"md instance m={m} cplx={cplx} it={it}")
+
+
+def test_batched_points_equal_single_points():
+    """one launch per layer across a batch of points == each point alone."""
+    rng = np.random.default_rng(42)
+    base = po.gen_benchmark("p1", 12, 4, seed=7)
+    B = 5
+    Q = base.P * base.m
+    top = base.stat.shape[2]
+    stat = np.empty((Q, B, top, 13))
+    refs = []
+    for b in range(B):
+        zb = po.gen_benchmark("p1", 12, 4, seed=1000 + b)
+        s = base.stat.copy()
+        s[:, :, 1 + base.N:] = zb.stat[:, :, 1 + base.N:]  # point b's inputs
+        stat[:, b] = s.reshape(Q, top, 13)
+        q = po.Problem(base.n, base.d, base.m, False, base.nvars, base.idx, None, s)
+        refs.append(po.evaluate(q, "port"))
+    vg, rep = dev_eval(base, stat)
+    for b in range(B):
+        assert_bitwise(vg[:, b].reshape(refs[b].shape), refs[b], f"point {b}")
+    assert rep.batch == B
+
+
+def test_errors_are_invalid_argument():
+    with pytest.raises(pe.InvalidArgument):
+        pe.evaluate_packed(2, 3, 7, "real", [1], [1], None, np.zeros((7, 1, 4, 4)))
+    with pytest.raises(pe.InvalidArgument):
+        pe.evaluate_packed(2, 3, 2, "real", [2], [2, 1], None, np.zeros((2, 1, 4, 4)))
