@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -81,8 +82,8 @@ struct Launchers {
 
 #ifdef PSE_KERNELS_IMPL
 
-constexpr int kConvThreads = 128;
-constexpr int kAddThreads = 128;
+constexpr int kConvThreads = kLaneThreads;
+constexpr int kAddThreads = kLaneThreads;
 
 template <int M>
 __device__ __forceinline__ void load_md(const double* __restrict__ src, int S, int j, double (&v)[M]) {
@@ -111,10 +112,19 @@ __device__ __forceinline__ void copy_md(double (&d)[M], const double (&s)[M]) {
 // acc = md_add(acc, x_i*y_{k-i}) -- the bit-exactness contract.
 // Consecutive lanes are consecutive pairs of one job: x_i is a broadcast
 // load and y_{k-i} a coalesced one.
-template <int M, bool CPLX>
-__global__ void __launch_bounds__(kConvThreads) k_conv(const ConvArgs a) {
+// MINB = resident blocks per SM the register allocation targets (4 -> 128
+// registers, 3 -> 168, 2 -> 255). Large M trade occupancy for the ILP that
+// ptxas only exposes with more registers; selectable at run time for tuning
+// (PSE_CONV_MINB), default from conv_default_minb<M>().
+template <int M>
+constexpr int conv_default_minb() {
+  return 4;
+}
+
+template <int M, bool CPLX, int MINB>
+__global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
   extern __shared__ double smem[];
-  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const Lane sm = make_lane(smem);
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * a.npairs;
   if (g >= ntasks) return;
@@ -142,52 +152,34 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(const ConvArgs a) {
 
   const int n1 = k1 + 1;
   const int total = k2 > k1 ? d + 2 : n1;
-  double ar[M], ai[M];   // accumulators (re, im)
-  double xr[M], yr[M];   // current operands (re)
-  double xi[M], yi[M];   // current operands (im, complex only)
-  load_md<M>(X, S, 0, xr);
-  load_md<M>(Y, S, k1, yr);
-  if constexpr (CPLX) {
-    load_md<M>(X + M * S, S, 0, xi);
-    load_md<M>(Y + M * S, S, k1, yi);
-  }
+  double ar[M], ai[M];  // accumulators (re, im)
 #pragma unroll 1
   for (int t = 0; t < total; ++t) {
     const bool second = t >= n1;
     const int kk = second ? k2 : k1;
     const int i = second ? t - n1 : t;
-    // next operands: (kk, i+1) or the start of the second chain
-    const int tn = t + 1;
-    const bool nsecond = tn >= n1;
-    const int ni = nsecond ? tn - n1 : tn;
-    const int nk = nsecond ? k2 : k1;
-    const bool more = tn < total;
     if constexpr (!CPLX) {
-      double p[M];
+      double xr[M], yr[M], p[M];
+      load_md<M>(X, S, i, xr);
+      load_md<M>(Y, S, kk - i, yr);
       exp_mul_fast<M>(xr, yr, p, sm);
-      if (more) {
-        load_md<M>(X, S, ni, xr);
-        load_md<M>(Y, S, nk - ni, yr);
-      }
       if (i == 0)
         copy_md<M>(ar, p);
       else
         exp_add_fast<M>(ar, p, ar, sm);
     } else {
       // (xr + i xi)(yr + i yi): pseries.cpp:50-51 operand order
-      double p1[M], p2[M], pre[M], pim[M];
+      double xr[M], yr[M], xi[M], yi[M], p1[M], p2[M], pre[M], pim[M];
+      load_md<M>(X, S, i, xr);
+      load_md<M>(Y, S, kk - i, yr);
+      load_md<M>(X + M * S, S, i, xi);
+      load_md<M>(Y + M * S, S, kk - i, yi);
       exp_mul_fast<M>(xr, yr, p1, sm);
       exp_mul_fast<M>(xi, yi, p2, sm);
       exp_sub_fast<M>(p1, p2, pre, sm);
       exp_mul_fast<M>(xr, yi, p1, sm);
       exp_mul_fast<M>(xi, yr, p2, sm);
       exp_add_fast<M>(p1, p2, pim, sm);
-      if (more) {
-        load_md<M>(X, S, ni, xr);
-        load_md<M>(Y, S, nk - ni, yr);
-        load_md<M>(X + M * S, S, ni, xi);
-        load_md<M>(Y + M * S, S, nk - ni, yi);
-      }
       if (i == 0) {
         copy_md<M>(ar, pre);
         copy_md<M>(ai, pim);
@@ -209,7 +201,7 @@ __global__ void __launch_bounds__(kConvThreads) k_conv(const ConvArgs a) {
 template <int M, bool CPLX>
 __global__ void __launch_bounds__(kAddThreads) k_add(const AddArgs a) {
   extern __shared__ double smem[];
-  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const Lane sm = make_lane(smem);
   const int d1 = a.G.d + 1;
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * d1;
@@ -238,7 +230,7 @@ __global__ void __launch_bounds__(kAddThreads) k_add(const AddArgs a) {
 template <int M, bool CPLX>
 __global__ void __launch_bounds__(kAddThreads) k_scale(const ScaleArgs a) {
   extern __shared__ double smem[];
-  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const Lane sm = make_lane(smem);
   const int d1 = a.G.d + 1;
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t ntasks = static_cast<int64_t>(a.batch) * a.nitems * d1;
@@ -268,7 +260,7 @@ __global__ void __launch_bounds__(kAddThreads) k_scale(const ScaleArgs a) {
 template <int M, bool CPLX>
 __global__ void __launch_bounds__(kAddThreads) k_extract(const ExtractArgs a) {
   extern __shared__ double smem[];
-  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const Lane sm = make_lane(smem);
   const int d1 = a.G.d + 1;
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t ntasks = static_cast<int64_t>(a.batch) * a.nrows * d1;
@@ -308,7 +300,7 @@ __global__ void __launch_bounds__(kAddThreads) k_extract(const ExtractArgs a) {
 template <int M>
 __global__ void __launch_bounds__(kAddThreads) k_md(const MdArgs a) {
   extern __shared__ double smem[];
-  const Lane sm{smem + threadIdx.x, static_cast<int>(blockDim.x)};
+  const Lane sm = make_lane(smem);
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= a.count) return;
   double x[M], y[M], z[M];
@@ -340,11 +332,25 @@ __global__ void __launch_bounds__(kAddThreads) k_md(const MdArgs a) {
 template <int M, bool CPLX>
 struct Impl {
   static size_t smem(int threads) { return static_cast<size_t>(threads) * MdTraits<M>::LANE * sizeof(double); }
+  static int minb() {
+    static const int v = [] {
+      const char* e = getenv("PSE_CONV_MINB");
+      const int x = e ? atoi(e) : conv_default_minb<M>();
+      return (x >= 2 && x <= 5) ? x : conv_default_minb<M>();
+    }();
+    return v;
+  }
   static void conv(const ConvArgs& a, cudaStream_t s) {
     const int64_t n = static_cast<int64_t>(a.batch) * a.njobs * a.npairs;
     if (n == 0) return;
     const size_t sh = smem(kConvThreads);
-    k_conv<M, CPLX><<<static_cast<unsigned>((n + kConvThreads - 1) / kConvThreads), kConvThreads, sh, s>>>(a);
+    const unsigned grid = static_cast<unsigned>((n + kConvThreads - 1) / kConvThreads);
+    switch (M >= 8 ? minb() : 4) {
+      case 2: k_conv<M, CPLX, 2><<<grid, kConvThreads, sh, s>>>(a); break;
+      case 3: k_conv<M, CPLX, 3><<<grid, kConvThreads, sh, s>>>(a); break;
+      case 5: k_conv<M, CPLX, 5><<<grid, kConvThreads, sh, s>>>(a); break;
+      default: k_conv<M, CPLX, 4><<<grid, kConvThreads, sh, s>>>(a); break;
+    }
   }
   static void add(const AddArgs& a, cudaStream_t s) {
     const int64_t n = static_cast<int64_t>(a.batch) * a.njobs * (a.G.d + 1);
@@ -371,7 +377,10 @@ struct Impl {
   }
   static void prepare() {
     const int c = static_cast<int>(smem(kConvThreads)), o = static_cast<int>(smem(kAddThreads));
-    cudaFuncSetAttribute(k_conv<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
+    cudaFuncSetAttribute(k_conv<M, CPLX, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
+    cudaFuncSetAttribute(k_conv<M, CPLX, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
+    cudaFuncSetAttribute(k_conv<M, CPLX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
+    cudaFuncSetAttribute(k_conv<M, CPLX, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_add<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
     cudaFuncSetAttribute(k_scale<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
     cudaFuncSetAttribute(k_extract<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);

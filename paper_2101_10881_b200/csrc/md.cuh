@@ -178,54 +178,111 @@ __device__ __noinline__ void exp_mul_lit(const double* x, const double* y, doubl
 }
 
 // ---------------------------------------------------------------- fast
-// A thread's private shared-memory lane, [index][thread] layout.
+// Every kernel that uses a lane runs kLaneThreads threads per block, so the
+// row pitch is a compile-time constant and lane addresses are one 32-bit
+// shared-memory register plus an immediate offset.
+constexpr int kLaneThreads = 128;
+constexpr unsigned kRow = kLaneThreads * sizeof(double);  // bytes between rows
+
+// A thread's private shared-memory lane: row r at byte address base + r*kRow.
 struct Lane {
-  double* p;
-  int stride;
-  __device__ __forceinline__ double& operator[](int i) const { return p[i * stride]; }
+  unsigned base;
 };
+
+__device__ __forceinline__ Lane make_lane(double* smem) {
+  return Lane{static_cast<unsigned>(__cvta_generic_to_shared(smem + threadIdx.x))};
+}
+
+// volatile: the stack's stores and loads must keep their program order
+__device__ __forceinline__ void sts64(unsigned addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v));
+}
+__device__ __forceinline__ double lds64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+// v != 0.0 (either sign) on the integer pipe: one LOP3 + one ISETP
+__device__ __forceinline__ bool nonzero(double v) {
+  return ((static_cast<unsigned>(__double2hiint(v)) & 0x7fffffffu) | static_cast<unsigned>(__double2loint(v))) != 0u;
+}
+
+// bitwise inequality accumulator: d |= bits(a) ^ bits(b)
+__device__ __forceinline__ unsigned diff_bits(double a, double b, unsigned d) {
+  return d | (static_cast<unsigned>(__double2loint(a)) ^ static_cast<unsigned>(__double2loint(b))) |
+         (static_cast<unsigned>(__double2hiint(a)) ^ static_cast<unsigned>(__double2hiint(b)));
+}
+
+// tighten (expansion.hpp:92-114). The reference writes (s, e) back only when
+// a bit differs; writing unconditionally is the same, because equal bits
+// leave the value unchanged. Only the "did anything change" flag needs the
+// comparison, accumulated with XOR/OR on the integer pipe.
+template <int M>
+__device__ __forceinline__ unsigned tighten_pass(double (&w)[M]) {
+  unsigned diff = 0;
+#pragma unroll
+  for (int i = 0; i + 1 < M; ++i) {
+    double s, e;
+    two_sum(w[i], w[i + 1], s, e);
+    diff = diff_bits(s, w[i], diff_bits(e, w[i + 1], diff));
+    w[i] = s;
+    w[i + 1] = e;
+  }
+  return diff;
+}
+
+// Passes 1 and 2 are straight-line code (a warp almost always needs both:
+// any of its 32 lanes still changing forces another pass); later passes loop.
+template <int M>
+__device__ __forceinline__ void tighten_fast(double (&w)[M]) {
+  if (tighten_pass<M>(w) == 0) return;
+  if (M == 2 || tighten_pass<M>(w) == 0) return;
+#pragma unroll 1
+  for (int pass = 2; pass < M; ++pass)
+    if (tighten_pass<M>(w) == 0) return;
+}
 
 template <int M>
 struct MdTraits {
   static constexpr int NT = M * (M + 1) + (M - 1);
-  // stack capacity for nonzero vec_sum pass-2 terms; the measured maximum
-  // over 2e5 random full-precision pairs is 39 (M=10) and 31 (M=8); small M
-  // reserve the full NT-1 so they can never overflow
-  static constexpr int CAP = M == 10 ? 48 : M == 8 ? 40 : (NT - 1 > 2 * M + 1 ? NT - 1 : 2 * M + 1);
-  // words per thread in the shared-memory lane (add merge needs 2M + 1)
-  static constexpr int LANE = CAP > 2 * M + 1 ? CAP : 2 * M + 1;
+  // Stack capacity for nonzero vec_sum pass-2 terms. The measured maximum over
+  // 2e5 random full-precision pairs is 39 (M=10) and 31 (M=8), the 99th
+  // percentile 31 and 24; small M reserve the full NT-1 so they never overflow.
+  static constexpr int CAP = M == 10 ? 43 : M == 8 ? 40 : NT - 1;
+  // rows per thread: CAP + one sacrificial row; the add merge reads up to row
+  // 2M+1 (look-ahead past the y block)
+  static constexpr int LANE = (CAP + 1 > 2 * M + 2) ? CAP + 1 : 2 * M + 2;
 };
 
-// out = x + y. Safe for out aliasing x or y (all reads precede writes).
+// out = x + y (expansion.hpp:142-158). Safe for out aliasing x or y.
 template <int M>
-__device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double (&y)[M], double (&out)[M],
-                                             Lane sm) {
+__device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double (&y)[M], double (&out)[M], Lane ln) {
   if constexpr (M == 1) {
     out[0] = __dadd_rn(x[0], y[0]);
   } else {
 #pragma unroll
     for (int q = 0; q < M; ++q) {
-      sm[q] = x[q];
-      sm[M + q] = y[q];
+      sts64(ln.base + q * kRow, x[q]);
+      sts64(ln.base + (M + q) * kRow, y[q]);
     }
-    // merge by magnitude, ties take x (expansion.hpp:150-153)
+    // merge by magnitude, ties take x (expansion.hpp:150-153); x and y
+    // heads live in registers, the refill comes from the lane
     double t[2 * M];
-    int i = 0, j = 0;
+    int i = 0;  // x elements taken; y taken = p - i
     double xh = x[0], yh = y[0];
+    unsigned xa = ln.base + kRow, ya = ln.base + (M + 1) * kRow;
 #pragma unroll
     for (int p = 0; p < 2 * M; ++p) {
-      const bool take_x = (j >= M) || (i < M && fabs(xh) >= fabs(yh));
+      const bool take_x = (p - i >= M) || (i < M && fabs(xh) >= fabs(yh));
       t[p] = take_x ? xh : yh;
       if (p + 1 < 2 * M) {
-        const int ni = take_x ? i + 1 : M + j + 1;  // index 2M is a readable spare word
-        const double v = sm[ni];
-        if (take_x) {
-          xh = v;
-          ++i;
-        } else {
-          yh = v;
-          ++j;
-        }
+        const double v = lds64(take_x ? xa : ya);
+        xh = take_x ? v : xh;
+        yh = take_x ? yh : v;
+        xa += take_x ? kRow : 0u;
+        ya += take_x ? 0u : kRow;
+        i += take_x ? 1 : 0;
       }
     }
     // vec_sum over 2M (expansion.hpp:61-69)
@@ -237,156 +294,185 @@ __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double 
       t[q + 1] = e;
     }
     t[0] = s;
-    // vec_sum_err_branch (expansion.hpp:74-90); emissions go to the lane
+    // vec_sum_err_branch (expansion.hpp:74-90); emission jj goes to row jj
     int jj = 0;
     double eps = t[0];
-    bool done = false;
 #pragma unroll
     for (int q = 1; q < 2 * M; ++q) {
-      if (!done) {
+      if (jj < M) {
         double r, tt;
         fast_two_sum(eps, t[q], r, tt);
-        if (tt != 0.0) {
-          sm[jj] = r;
-          ++jj;
-          if (jj == M) done = true;
-          eps = tt;
-        } else {
-          eps = r;
-        }
+        const bool emit = nonzero(tt);
+        if (emit) sts64(ln.base + jj * kRow, r);
+        jj += emit ? 1 : 0;
+        eps = emit ? tt : r;
       }
     }
 #pragma unroll
     for (int q = 0; q < M; ++q) {
-      const double v = sm[q];
+      double v = 0.0;
+      if (q < jj) v = lds64(ln.base + q * kRow);
       out[q] = q < jj ? v : (q == jj ? eps : 0.0);
     }
-    tighten<M>(out);
+    tighten_fast<M>(out);
   }
 }
 
 template <int M>
-__device__ __forceinline__ void exp_sub_fast(const double (&x)[M], const double (&y)[M], double (&out)[M],
-                                             Lane sm) {
+__device__ __forceinline__ void exp_sub_fast(const double (&x)[M], const double (&y)[M], double (&out)[M], Lane ln) {
   if constexpr (M == 1) {
     out[0] = __dsub_rn(x[0], y[0]);
   } else {
     double ny[M];
 #pragma unroll
     for (int q = 0; q < M; ++q) ny[q] = -y[q];
-    exp_add_fast<M>(x, ny, out, sm);
+    exp_add_fast<M>(x, ny, out, ln);
   }
 }
 
 namespace detail {
 
-// streaming state of the two backward vec_sum passes
+// Streaming state of the two backward vec_sum passes and the compacted
+// stack of nonzero pass-2 outputs (top = byte address of the next free row).
 struct Passes {
   double s1, s2;
-  int sp;
-  bool ovf;
+  unsigned top;
 };
 
-template <int CAP>
-__device__ __forceinline__ void push_nonzero(Passes& st, double v, Lane sm) {
-  if (v != 0.0) {
-    if (st.sp < CAP)
-      sm[st.sp] = v;
-    else
-      st.ovf = true;
-    ++st.sp;
-  }
+// push v if nonzero; `clamp` (pushes beyond the first CAP) redirects the
+// store to the sacrificial row lim once the stack is full -- overflow is then
+// detected from the count and handled by the literal slow path
+template <bool CLAMP>
+__device__ __forceinline__ void push(Passes& st, double v, unsigned lim) {
+  sts64(CLAMP ? min(st.top, lim) : st.top, v);
+  st.top += nonzero(v) ? kRow : 0u;
 }
 
-// pass-2 step on x1 value v (x1 arrives x1[n-1], x1[n-2], ...)
-template <int CAP>
-__device__ __forceinline__ void feed2(Passes& st, double v, Lane sm) {
-  double e;
-  two_sum(v, st.s2, st.s2, e);
-  push_nonzero<CAP>(st, e, sm);
-}
-
-// pass-1 step on term t (terms arrive t[n-2], t[n-3], ..., t[0])
-template <int CAP>
-__device__ __forceinline__ void feed(Passes& st, double t, Lane sm) {
-  double e;
-  two_sum(t, st.s1, st.s1, e);
-  feed2<CAP>(st, e, sm);
+// pass-1 step on term t (terms arrive t[n-2], t[n-3], ..., t[0]) followed by
+// the pass-2 step on the error it produces (x1 arrives x1[n-1], x1[n-2], ...)
+template <bool CLAMP>
+__device__ __forceinline__ void feed(Passes& st, double t, unsigned lim) {
+  double e1, e2;
+  two_sum(t, st.s1, st.s1, e1);
+  two_sum(e1, st.s2, st.s2, e2);
+  push<CLAMP>(st, e2, lim);
 }
 
 }  // namespace detail
 
 // out = x * y (expansion.hpp:177-211), register-streamed; see file header.
-// Safe for out aliasing x or y only if the caller copies first (x, y are read
-// until the end of term generation).
 template <int M>
-__device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double (&y)[M], double (&out)[M],
-                                             Lane sm) {
+__device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double (&y)[M], double (&out)[M], Lane ln) {
   if constexpr (M == 1) {
     out[0] = __dmul_rn(x[0], y[0]);
   } else {
     constexpr int CAP = MdTraits<M>::CAP;
+    const unsigned lim = ln.base + CAP * kRow;
     detail::Passes st;
-    st.sp = 0;
-    st.ovf = false;
+    st.top = ln.base;
+    // Pass 2 runs one term behind pass 1: the pass-1 error of term i is
+    // consumed by pass 2 while pass 1 processes term i+1, so the two
+    // two_sums of a step are independent and interleave (ILP 2). The
+    // sequence of operations on each pass is unchanged.
+    int fed = 0;      // compile-time after unrolling
+    int pushes = 0;
+    double e1p = 0.0; // pending pass-1 error (next pass-2 input)
+    auto feed = [&](double t) {
+      if (fed == 0) {
+        st.s1 = t;  // t[NT-1] seeds pass 1
+      } else if (fed == 1) {
+        two_sum(t, st.s1, st.s1, st.s2);  // x1[NT-1] seeds pass 2
+      } else if (fed == 2) {
+        two_sum(t, st.s1, st.s1, e1p);
+      } else {
+        double e1, e2;
+        two_sum(t, st.s1, st.s1, e1);
+        two_sum(e1p, st.s2, st.s2, e2);
+        if (pushes < CAP)
+          detail::push<false>(st, e2, lim);
+        else
+          detail::push<true>(st, e2, lim);
+        ++pushes;
+        e1p = e1;
+      }
+      ++fed;
+    };
     // Reverse term order: section k (k = M..1) = [errors of diagonal k-1,
     // reversed] then [products of diagonal k, reversed]; finally diagonal 0.
+    // One diagonal of products is held while the next diagonal's errors are
+    // fed.
     double pr[M];
     {
       double er[M];
 #pragma unroll
       for (int i = 0; i < M; ++i) two_prod(x[i], y[M - 1 - i], pr[i], er[i]);
-      st.s1 = er[M - 1];  // t[NT-1] seeds pass 1
-      double e;
-      two_sum(er[M - 2], st.s1, st.s1, e);
-      st.s2 = e;  // x1[NT-1] seeds pass 2
 #pragma unroll
-      for (int i = M - 3; i >= 0; --i) detail::feed<CAP>(st, er[i], sm);
+      for (int i = M - 1; i >= 0; --i) feed(er[i]);
     }
     // diagonal M: plain products (expansion.hpp:197-200)
 #pragma unroll
-    for (int i = M - 1; i >= 1; --i) detail::feed<CAP>(st, __dmul_rn(x[i], y[M - i]), sm);
+    for (int i = M - 1; i >= 1; --i) feed(__dmul_rn(x[i], y[M - i]));
 #pragma unroll
     for (int k = M - 1; k >= 1; --k) {
       double pn[M], en[M];
 #pragma unroll
       for (int i = 0; i < k; ++i) two_prod(x[i], y[k - 1 - i], pn[i], en[i]);
 #pragma unroll
-      for (int i = k - 1; i >= 0; --i) detail::feed<CAP>(st, en[i], sm);
+      for (int i = k - 1; i >= 0; --i) feed(en[i]);
 #pragma unroll
-      for (int i = k; i >= 0; --i) detail::feed<CAP>(st, pr[i], sm);
+      for (int i = k; i >= 0; --i) feed(pr[i]);
 #pragma unroll
       for (int i = 0; i < k; ++i) pr[i] = pn[i];
     }
-    detail::feed<CAP>(st, pr[0], sm);  // t[0]
-    detail::feed2<CAP>(st, st.s1, sm); // x1[0] = pass-1 sum
-    // st.s2 = x2[0]; stack holds nonzero x2[NT-1..1], top = x2[1]
-    int jj = 0;
-    double eps = st.s2;
-    if (!st.ovf) {
-      // vec_sum_err_branch over the compacted terms; emission jj is written
-      // into a stack word that has already been popped
-      int q = st.sp - 1;
-      while (q >= 0) {
-        const double v = sm[q];
-        double r, tt;
-        fast_two_sum(eps, v, r, tt);
-        if (tt != 0.0) {
-          sm[st.sp - 1 - jj] = r;
-          ++jj;
-          if (jj == M) break;
-          eps = tt;
-        } else {
-          eps = r;
+    feed(pr[0]);  // t[0]
+    {             // drain pass 2: x1[1] (pending), then x1[0] = the pass-1 sum
+      double e;
+      two_sum(e1p, st.s2, st.s2, e);
+      detail::push<true>(st, e, lim);
+      two_sum(st.s1, st.s2, st.s2, e);
+      detail::push<true>(st, e, lim);
+    }
+    // st.s2 = x2[0]; rows [0, count) hold the nonzero x2[NT-1..1], x2[1] on top
+    const int count = static_cast<int>((st.top - ln.base) / kRow);
+    if (count <= CAP) {
+      // vec_sum_err_branch over the compacted terms (popped top-down, one
+      // row of look-ahead); emission jj overwrites row count-1-jj, which has
+      // already been consumed
+      // Four pops per trip; each step is predicated on "still below M
+      // emissions and terms left", so a lane that finished mid-trip is inert.
+      int jj = 0;
+      double eps = st.s2;
+      unsigned a = st.top;               // one past the next row to pop
+      unsigned ea = st.top - kRow;       // row for emission jj
+      const unsigned bottom = ln.base;   // popping stops at row 0
+#pragma unroll 1
+      while (jj < M && a > bottom) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = lds64(static_cast<unsigned>(max(static_cast<int>(a) - (u + 1) * static_cast<int>(kRow),
+                                                 static_cast<int>(bottom))));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (jj < M && a > bottom) {
+            double r, tt;
+            fast_two_sum(eps, v[u], r, tt);
+            const bool emit = nonzero(tt);
+            if (emit) sts64(ea, r);
+            ea -= emit ? kRow : 0u;
+            jj += emit ? 1 : 0;
+            eps = emit ? tt : r;
+            a -= kRow;
+          }
         }
-        --q;
       }
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        const double v = sm[st.sp - 1 - k < 0 ? 0 : st.sp - 1 - k];
+        double v = 0.0;
+        if (k < jj) v = lds64(st.top - (k + 1) * kRow);
         out[k] = k < jj ? v : (k == jj ? eps : 0.0);
       }
-      tighten<M>(out);
+      tighten_fast<M>(out);
     } else {
       // rare: more nonzero terms than the lane holds -> literal algorithm
       double xl[M], yl[M], ol[M];

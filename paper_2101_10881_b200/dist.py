@@ -1,0 +1,84 @@
+"""Multi-GPU plumbing: one process per GPU, torch.distributed for the
+barrier / timing reductions only.
+
+The evaluation of independent points shards with no
+data-path collective: each rank owns a contiguous range of points, keeps the
+graph and coefficient slabs replicated, and produces bit-identical results to
+a single GPU. Partial value/gradient series are never summed with NCCL's
+native sum (it would add limbs as plain doubles); when one consumer needs all
+points, ``gather_points`` moves the finished series with an all-gather.
+"""
+from __future__ import annotations
+
+import os
+from typing import Tuple
+
+
+def env_rank() -> Tuple[int, int, int]:
+    """(rank, local_rank, world_size) from the torchrun environment."""
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def point_range(total: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous [begin, end) share of `total` points for `rank`; sizes differ
+    by at most one, lower ranks take the remainder."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, rem = divmod(total, world)
+    begin = rank * base + min(rank, rem)
+    return begin, begin + base + (1 if rank < rem else 0)
+
+
+def init(backend: str):
+    import torch.distributed as dist
+
+    if dist.is_available() and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return dist
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def gather_points(local, total: int, device=None):
+    """All-gather per-rank blocks of finished series along axis 1 (points).
+    local: numpy [Q][points_local][...]; returns numpy [Q][total][...].
+    A pure data movement: no arithmetic is applied to the limbs."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return local
+    world = dist.get_world_size()
+    rows = [point_range(total, r, world) for r in range(world)]
+    width = max(e - b for b, e in rows)
+    shape = (local.shape[0], width) + tuple(local.shape[2:])
+    buf = np.zeros(shape, np.float64)
+    buf[:, : local.shape[1]] = local
+    t = torch.from_numpy(buf).to(device) if device is not None else torch.from_numpy(buf)
+    outs = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(outs, t)
+    parts = [o.cpu().numpy()[:, : e - b] for o, (b, e) in zip(outs, rows)]
+    return np.concatenate(parts, axis=1)

@@ -191,6 +191,38 @@ class JobGraph:
         return out
 
 
+class GraphArrays:
+    """A pse_graph_desc over caller-owned numpy arrays (e.g. a JobGraph read
+    back, edited, and handed to validate() or a DevicePlan)."""
+
+    def __init__(self, n, N, d, total_slots, value_slot, gradient_slots, multipliers, conv_layer_off, conv_in1,
+                 conv_in2, conv_out, conv_copy, add_layer_off, add_src, add_dst, ts_slot=(), ts_factor=()):
+        i64 = lambda a: np.ascontiguousarray(a, np.int64)
+        self._keep = dict(gs=i64(gradient_slots), mu=i64(multipliers), co=i64(conv_layer_off), c1=i64(conv_in1),
+                          c2=i64(conv_in2), c3=i64(conv_out), cc=np.ascontiguousarray(conv_copy, np.uint8),
+                          ao=i64(add_layer_off), a1=i64(add_src), a2=i64(add_dst), t1=i64(ts_slot), t2=i64(ts_factor))
+        k = self._keep
+        P64, P8 = C.POINTER(C.c_int64), C.POINTER(C.c_uint8)
+        p = lambda a, t=P64: a.ctypes.data_as(t)
+        self.n, self.N, self.d, self.total_slots = n, N, d, total_slots
+        self.desc_base = dict(n=n, N=N, d=d, total_slots=total_slots, value_slot=value_slot, gradient_slots=p(k["gs"]),
+                              multipliers=p(k["mu"]), n_conv_layers=len(k["co"]) - 1, conv_layer_off=p(k["co"]),
+                              conv_in1=p(k["c1"]), conv_in2=p(k["c2"]), conv_out=p(k["c3"]), conv_copy=p(k["cc"], P8),
+                              n_add_layers=len(k["ao"]) - 1, add_layer_off=p(k["ao"]), add_src=p(k["a1"]),
+                              add_dst=p(k["a2"]), n_term_scales=len(k["t1"]), ts_slot=p(k["t1"]), ts_factor=p(k["t2"]))
+
+    @classmethod
+    def from_graph(cls, g: "JobGraph"):
+        return cls(g.n, g.N, g.d, g.total_slots, g.value_slot, g.gradient_slots, g.multipliers, g.conv_layer_off,
+                   g.conv_in1, g.conv_in2, g.conv_out, g.conv_copy, g.add_layer_off, g.add_src, g.add_dst,
+                   g.term_scales[:, 0], g.term_scales[:, 1])
+
+    def desc(self, m: int, mode: str) -> GraphDesc:
+        d = GraphDesc(**self.desc_base)
+        d.m, d.mode = m, _mode_code(mode)
+        return d
+
+
 def build_jobgraph_shape(n: int, d: int, nvars, indices, exponents=None) -> JobGraph:
     nv = np.ascontiguousarray(nvars, np.int32)
     ix = np.ascontiguousarray(indices, np.int32)

@@ -186,3 +186,19 @@ def test_errors_are_invalid_argument():
         pe.evaluate_packed(2, 3, 7, "real", [1], [1], None, np.zeros((7, 1, 4, 4)))
     with pytest.raises(pe.InvalidArgument):
         pe.evaluate_packed(2, 3, 2, "real", [2], [2, 1], None, np.zeros((2, 1, 4, 4)))
+
+
+def test_reference_binding_drop_in():
+    """include/pse_b200_pseval.hpp compiled against the unmodified reference
+    sources: run_device == run_sequential bit for bit on the reference's own
+    DataArray (oracle/integration_check.cpp; built where /root/reference was
+    available)."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(po.__file__), "_ref", "integration_check")
+    if not os.path.exists(exe):
+        pytest.skip("integration_check not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK: 4/4" in r.stdout

@@ -1,5 +1,6 @@
-import sys, time, numpy as np
-sys.path.insert(0, 'oracle')
+import os, sys, time, numpy as np
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 'oracle'))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2101_10881_b200 as pe
 print(pe.device_info())
 print('fp64 peak', pe.fp64_peak())
