@@ -93,7 +93,7 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+                 "-lms", "50", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         return self
@@ -209,10 +209,14 @@ def ours(args, wl):
     from paper_2101_10881_b200 import dist as D
 
     rank, local, world = D.env_rank()
+    dev = local % max(1, torch.cuda.device_count())
+    # NCCL for the barrier / max-over-ranks timing reduction; PSE_DIST_BACKEND
+    # =gloo lets several ranks share one GPU when testing the multi-rank path
+    backend = os.environ.get("PSE_DIST_BACKEND", "nccl")
+    red_dev = torch.device(f"cuda:{dev}") if backend == "nccl" else None
     if world > 1:
-        torch.cuda.set_device(local)
-        D.init("nccl")
-    dev = local
+        torch.cuda.set_device(dev)
+        D.init(backend)
     pid, d, m, ppg, desc = WORKLOADS[wl]
     total_points = ppg * world if wl != "c5" else ppg
     b0, b1 = D.point_range(total_points, rank, world)
@@ -270,7 +274,7 @@ def ours(args, wl):
     if world > 1:
         torch.distributed.barrier()
     my_total = sum(walls)
-    total_ms = D.max_over_ranks(my_total, torch.device(f"cuda:{dev}"))
+    total_ms = D.max_over_ranks(my_total, red_dev)
     ms_per_step = total_ms / args.steps
     value = model_ops * total_points * args.steps / (total_ms * 1e-3) / 1e12
     conv_ms = sum(convs)
@@ -297,8 +301,8 @@ def ours(args, wl):
         _, _, rep = plan.run(pin_in, nb, out=pin_out)
         if s >= args.warmup:
             e2e_ms.append(rep.e2e_ms)
-    e2e_total = D.max_over_ranks(sum(e2e_ms), torch.device(f"cuda:{dev}"))
-    e2e_points = nb * D.sum_over_ranks(1.0, torch.device(f"cuda:{dev}"))
+    e2e_total = D.max_over_ranks(sum(e2e_ms), red_dev)
+    e2e_points = nb * D.sum_over_ranks(1.0, red_dev)
     e2e_value = model_ops * e2e_points * args.steps / (e2e_total * 1e-3) / 1e12
     lib().pse_host_free(hin)
     lib().pse_host_free(hout)
@@ -342,7 +346,7 @@ def ours(args, wl):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -129,8 +130,20 @@ struct Plan {
   int max_batch = 1;
   Geom G{};
   const Launchers* L = nullptr;
-  // layer job tables on the device
-  std::vector<std::pair<int4*, int>> conv_layers;  // (jobs, njobs)
+  // Conv stage. Prologue layers (device exponent folding) run first on the
+  // main stream; the graph's own conv jobs are partitioned into independent
+  // groups (connected components of their dynamic slots, i.e. sets of whole
+  // monomials) whose layer sequences run concurrently on their own streams.
+  struct ConvGroup {
+    std::vector<std::pair<int4*, int>> layers;  // (jobs, njobs) per layer
+    cudaStream_t stream = nullptr;
+    cudaEvent_t join = nullptr;
+    double* prod = nullptr;  // split-path scratch of this group
+    int64_t prod_words = 0;
+  };
+  std::vector<std::pair<int4*, int>> pro_layers;
+  std::vector<ConvGroup> groups;
+  cudaEvent_t fork = nullptr;
   std::vector<std::pair<int2*, int>> add_layers;
   int2* ts = nullptr;
   int nts = 0;
@@ -143,6 +156,10 @@ struct Plan {
   double* stage = nullptr;  // [Q][max_batch][top][d+1]
   double* vg = nullptr;     // [Q][max_batch][n+1][d+1]
   double* dyn = nullptr;    // lazily: [Q][max_batch][TS][d+1]
+  // split-convolution index table (k, i) of the triangular product index
+  int2* tri = nullptr;
+  int T = 0;
+  int64_t split_threshold = 0;
   // accounting (per point)
   int64_t flops_model = 0, alg_ops = 0, conv_jobs = 0, add_jobs = 0, copy_jobs = 0;
   std::map<int, cudaGraphExec_t> graphs;
@@ -157,17 +174,55 @@ struct Plan {
     cudaFree(stage);
     cudaFree(vg);
     cudaFree(dyn);
+    cudaFree(tri);
+    for (ConvGroup& gr : groups) {
+      cudaFree(gr.prod);
+      if (gr.join) cudaEventDestroy(gr.join);
+      if (gr.stream) cudaStreamDestroy(gr.stream);
+    }
+    if (fork) cudaEventDestroy(fork);
     if (stream) cudaStreamDestroy(stream);
   }
 
   // launch the whole phase sequence; if ts is non-null, record an event
   // after every phase into ts (conv layers, scale, add layers, extract)
+  // A conv layer runs split (products in parallel, then the accumulation
+  // chains) when one thread per coefficient pair cannot fill the GPU.
+  // The threshold is per group: concurrent groups share the GPU.
+  bool split_layer(int nj, int batch, const ConvGroup& gr) const {
+    return gr.prod != nullptr &&
+           static_cast<int64_t>(batch) * nj * ((d + 2) / 2) * static_cast<int64_t>(groups.size()) < split_threshold &&
+           static_cast<int64_t>(batch) * nj * T * Q <= gr.prod_words;
+  }
+
+  int launch_layer(int4* jobs, int nj, int batch, const ConvGroup& gr, cudaStream_t st) {
+    if (split_layer(nj, batch, gr)) {
+      SplitArgs a{arena, G, jobs, nj, batch, gr.prod, tri, T};
+      L->conv_prod(a, st);
+      L->conv_accum(a, st);
+      return 2;
+    }
+    ConvArgs a{arena, G, jobs, nj, (d + 2) / 2, batch};
+    L->conv(a, st);
+    return 1;
+  }
+
   int launch_all(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
     int launches = 0;
-    for (auto& [jobs, nj] : conv_layers) {
-      ConvArgs a{arena, G, jobs, nj, (d + 2) / 2, batch};
-      L->conv(a, stream);
-      ++launches;
+    for (auto& [jobs, nj] : pro_layers) launches += launch_layer(jobs, nj, batch, groups[0], stream);
+    if (groups.size() == 1) {
+      for (auto& [jobs, nj] : groups[0].layers) {
+        launches += launch_layer(jobs, nj, batch, groups[0], stream);
+        if (marks) mark(marks, 'c');
+      }
+    } else {
+      ck(cudaEventRecord(fork, stream), "fork");
+      for (ConvGroup& gr : groups) {
+        ck(cudaStreamWaitEvent(gr.stream, fork, 0), "fork wait");
+        for (auto& [jobs, nj] : gr.layers) launches += launch_layer(jobs, nj, batch, gr, gr.stream);
+        ck(cudaEventRecord(gr.join, gr.stream), "join");
+        ck(cudaStreamWaitEvent(stream, gr.join, 0), "join wait");
+      }
       if (marks) mark(marks, 'c');
     }
     if (nts) {
@@ -204,8 +259,12 @@ struct Plan {
     }
   }
 
-  int phase_count() const {
-    return static_cast<int>(conv_layers.size()) + (nts ? 1 : 0) + static_cast<int>(add_layers.size()) + 1;
+  int kernel_count(int batch) const {
+    int n = (nts ? 1 : 0) + static_cast<int>(add_layers.size()) + 1;
+    for (auto& [jobs, nj] : pro_layers) n += split_layer(nj, batch, groups[0]) ? 2 : 1;
+    for (const ConvGroup& gr : groups)
+      for (auto& [jobs, nj] : gr.layers) n += split_layer(nj, batch, gr) ? 2 : 1;
+    return n;
   }
 };
 
@@ -280,15 +339,80 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
   p->G.point_words = p->TSdev * p->G.slot_words;
 
   cudaStream_t s = p->stream;
-  for (auto& rows : layers) {
-    if (rows.empty()) continue;
+  auto upload_rows = [&](const std::vector<ConvRow>& rows) {
     std::vector<int4> v;
     v.reserve(rows.size());
     for (auto& r : rows)
       v.push_back(make_int4(static_cast<int>(r.in1), static_cast<int>(r.in2), static_cast<int>(r.out), r.copy));
     int4* dv = dev_upload(v, s);
     p->owned.push_back(dv);
-    p->conv_layers.emplace_back(dv, static_cast<int>(v.size()));
+    return std::make_pair(dv, static_cast<int>(v.size()));
+  };
+  const size_t npro = prologue.size();
+  for (size_t L = 0; L < npro; ++L)
+    if (!layers[L].empty()) p->pro_layers.push_back(upload_rows(layers[L]));
+
+  // Independent job groups: union-find over dynamic slots (>= top) of every
+  // non-prologue conv job; components (whole monomials) are dealt out in
+  // contiguous ranges of first appearance, balanced by job count.
+  {
+    std::map<int64_t, int64_t> parent;
+    std::function<int64_t(int64_t)> find = [&](int64_t x) {
+      auto it = parent.find(x);
+      if (it == parent.end()) {
+        parent[x] = x;
+        return x;
+      }
+      if (it->second == x) return x;
+      const int64_t r = find(it->second);
+      parent[x] = r;
+      return r;
+    };
+    auto unite = [&](int64_t a, int64_t b) {
+      a = find(a);
+      b = find(b);
+      if (a != b) parent[a] = b;
+    };
+    const int64_t top = p->top;
+    int64_t njobs = 0;
+    for (size_t L = npro; L < layers.size(); ++L)
+      for (const ConvRow& r : layers[L]) {
+        find(r.out);
+        if (r.in1 >= top) unite(r.in1, r.out);
+        if (!r.copy && r.in2 >= top) unite(r.in2, r.out);
+        ++njobs;
+      }
+    std::map<int64_t, int64_t> comp_jobs;  // root -> jobs
+    std::vector<int64_t> comp_order;
+    for (size_t L = npro; L < layers.size(); ++L)
+      for (const ConvRow& r : layers[L]) {
+        const int64_t c = find(r.out);
+        if (!comp_jobs.count(c)) comp_order.push_back(c);
+        ++comp_jobs[c];
+      }
+    const char* env = getenv("PSE_CONV_GROUPS");
+    int ng = env ? atoi(env) : 4;
+    ng = std::max(1, std::min<int>(ng, static_cast<int>(comp_order.size())));
+    std::map<int64_t, int> comp_group;
+    int64_t acc = 0;
+    for (int64_t c : comp_order) {
+      comp_group[c] = static_cast<int>(std::min<int64_t>(ng - 1, acc * ng / std::max<int64_t>(1, njobs)));
+      acc += comp_jobs[c];
+    }
+    p->groups.resize(ng);
+    for (size_t L = npro; L < layers.size(); ++L) {
+      std::vector<std::vector<ConvRow>> per(ng);
+      for (const ConvRow& r : layers[L]) per[comp_group[find(r.out)]].push_back(r);
+      for (int gi = 0; gi < ng; ++gi)
+        if (!per[gi].empty()) p->groups[gi].layers.push_back(upload_rows(per[gi]));
+    }
+    if (ng > 1) {
+      ck(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming), "event");
+      for (auto& gr : p->groups) {
+        ck(cudaStreamCreateWithFlags(&gr.stream, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreateWithFlags(&gr.join, cudaEventDisableTiming), "event");
+      }
+    }
   }
   for (int32_t L = 0; L < g.n_add_layers; ++L) {
     std::vector<int2> v;
@@ -323,6 +447,47 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
   p->row_mult = dev_upload(rm, s);
   p->owned.push_back(p->row_slot);
   p->owned.push_back(p->row_mult);
+
+  // Split-convolution scratch: sized for the largest (batch x layer) that
+  // the threshold sends down the split path, capped at 4 GiB (layers beyond
+  // the cap simply stay fused). Threshold: two waves of resident threads
+  // (4 blocks of 128 per SM); PSE_SPLIT_THRESHOLD overrides, 0 disables.
+  {
+    const char* env = getenv("PSE_SPLIT_THRESHOLD");
+    p->split_threshold = env ? atoll(env) : int64_t(p->sms) * 4 * 128 * 2;
+    p->T = (g.d + 1) * (g.d + 2) / 2;
+    const int64_t npairs = (g.d + 2) / 2, ng = static_cast<int64_t>(p->groups.size());
+    auto words_for = [&](const std::vector<std::pair<int4*, int>>& ls) {
+      int64_t need = 0;
+      for (auto& [jobs, nj] : ls) {
+        int64_t bmax = 0;
+        for (int b = max_batch; b >= 1; --b)
+          if (int64_t(b) * nj * npairs * ng < p->split_threshold) {
+            bmax = b;
+            break;
+          }
+        need = std::max(need, bmax * nj * int64_t(p->T) * p->Q);
+      }
+      return std::min<int64_t>(need, (int64_t(4) << 30) / 8 / ng);
+    };
+    bool any = false;
+    for (size_t gi = 0; gi < p->groups.size(); ++gi) {
+      Plan::ConvGroup& gr = p->groups[gi];
+      int64_t need = words_for(gr.layers);
+      if (gi == 0) need = std::max(need, words_for(p->pro_layers));
+      if (need > 0) {
+        gr.prod = dev_alloc<double>(static_cast<size_t>(need));
+        gr.prod_words = need;
+        any = true;
+      }
+    }
+    if (any) {
+      std::vector<int2> tri(p->T);
+      for (int k = 0, o = 0; k <= g.d; ++k)
+        for (int i = 0; i <= k; ++i) tri[o++] = make_int2(k, i);
+      p->tri = dev_upload(tri, s);
+    }
+  }
 
   p->arena = dev_alloc<double>(static_cast<size_t>(max_batch) * p->G.point_words);
   p->stage = dev_alloc<double>(static_cast<size_t>(p->Q) * max_batch * p->top * (g.d + 1));
@@ -413,7 +578,7 @@ int execute(Plan& p, int batch, int detail, pse_report* rep) {
     ck(cudaGraphLaunch(it->second, p.stream), "graph launch");
     ck(cudaEventRecord(p.ev[1], p.stream), "event");
     ck(cudaEventSynchronize(p.ev[1]), "execute");
-    launches = p.phase_count();
+    launches = p.kernel_count(batch);
     if (rep) {
       float ms = 0;
       ck(cudaEventElapsedTime(&ms, p.ev[0], p.ev[1]), "elapsed");

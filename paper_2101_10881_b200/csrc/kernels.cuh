@@ -70,8 +70,26 @@ struct MdArgs {
   double* out;
 };
 
+// Split convolution for layers too small to fill the GPU with one thread per
+// coefficient pair: every product x_i*y_{k-i} of the layer is computed
+// independently (conv_prod), then each coefficient's ascending-i md_add chain
+// runs over the stored products (conv_accum). The operation order of conv()
+// is unchanged, so the result is bit-identical to the fused kernel.
+struct SplitArgs {
+  double* arena;
+  Geom G;
+  const int4* jobs;
+  int njobs;
+  int batch;
+  double* prod;          // scratch: [point][job][T][Q], T = (d+1)(d+2)/2
+  const int2* tri;       // [T] (k, i) of triangular product index k(k+1)/2 + i
+  int T;
+};
+
 struct Launchers {
   void (*conv)(const ConvArgs&, cudaStream_t);
+  void (*conv_prod)(const SplitArgs&, cudaStream_t);
+  void (*conv_accum)(const SplitArgs&, cudaStream_t);
   void (*add)(const AddArgs&, cudaStream_t);
   void (*scale)(const ScaleArgs&, cudaStream_t);
   void (*extract)(const ExtractArgs&, cudaStream_t);
@@ -192,6 +210,111 @@ __global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
       store_md<M>(Z, S, kk, ar);
       if constexpr (CPLX) store_md<M>(Z + M * S, S, kk, ai);
     }
+  }
+}
+
+// ------------------------------------------------ split convolution (small)
+// Phase A: one thread per (point, job, product index). The product of a
+// complex coefficient pair is the (re, im) pair conv() adds to its
+// accumulators: sub(mul(re,re), mul(im,im)), add(mul(re,im), mul(im,re)).
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kConvThreads) k_conv_prod(const SplitArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm = make_lane(smem);
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * a.T;
+  if (g >= ntasks) return;
+  const int off = static_cast<int>(g % a.T);
+  const int64_t r = g / a.T;
+  const int jb = static_cast<int>(r % a.njobs);
+  const int64_t pt = r / a.njobs;
+  const int4 J = a.jobs[jb];
+  if (J.w) return;  // copy jobs have no products
+  const int2 ki = a.tri[off];
+  const int S = a.G.S;
+  constexpr int Q = CPLX ? 2 * M : M;
+  const double* base = a.arena + pt * a.G.point_words;
+  const double* X = base + static_cast<int64_t>(J.x) * a.G.slot_words;
+  const double* Y = base + static_cast<int64_t>(J.y) * a.G.slot_words;
+  double* P = a.prod + (r * a.T + off) * Q;
+  double xr[M], yr[M], p[M];
+  load_md<M>(X, S, ki.y, xr);
+  load_md<M>(Y, S, ki.x - ki.y, yr);
+  if constexpr (!CPLX) {
+    exp_mul_fast<M>(xr, yr, p, sm);
+#pragma unroll
+    for (int q = 0; q < M; ++q) P[q] = p[q];
+  } else {
+    double xi[M], yi[M], p2[M], pim[M];
+    load_md<M>(X + M * S, S, ki.y, xi);
+    load_md<M>(Y + M * S, S, ki.x - ki.y, yi);
+    exp_mul_fast<M>(xr, yr, p, sm);
+    exp_mul_fast<M>(xi, yi, p2, sm);
+    exp_sub_fast<M>(p, p2, p, sm);
+#pragma unroll
+    for (int q = 0; q < M; ++q) P[q] = p[q];
+    exp_mul_fast<M>(xr, yi, p, sm);
+    exp_mul_fast<M>(xi, yr, p2, sm);
+    exp_add_fast<M>(p, p2, pim, sm);
+#pragma unroll
+    for (int q = 0; q < M; ++q) P[M + q] = pim[q];
+  }
+}
+
+// Phase B: one thread per (point, job, coefficient pair), the same pairing
+// as k_conv; acc = P(k,0), acc = md_add(acc, P(k,i)) for ascending i.
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kConvThreads) k_conv_accum(const SplitArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm = make_lane(smem);
+  const int npairs = (a.G.d + 2) / 2;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * npairs;
+  if (g >= ntasks) return;
+  const int pair = static_cast<int>(g % npairs);
+  const int64_t r = g / npairs;
+  const int jb = static_cast<int>(r % a.njobs);
+  const int64_t pt = r / a.njobs;
+  const int4 J = a.jobs[jb];
+  const int S = a.G.S, d = a.G.d;
+  constexpr int Q = CPLX ? 2 * M : M;
+  double* base = a.arena + pt * a.G.point_words;
+  double* Z = base + static_cast<int64_t>(J.z) * a.G.slot_words;
+  const int k1 = pair, k2 = d - pair;
+  if (J.w) {
+    const double* X = base + static_cast<int64_t>(J.x) * a.G.slot_words;
+#pragma unroll 1
+    for (int q = 0; q < Q; ++q) {
+      Z[q * S + k1] = X[q * S + k1];
+      if (k2 != k1) Z[q * S + k2] = X[q * S + k2];
+    }
+    return;
+  }
+  const double* P = a.prod + r * a.T * Q;
+#pragma unroll 1
+  for (int c = 0; c < (k2 != k1 ? 2 : 1); ++c) {
+    const int k = c ? k2 : k1;
+    const double* Pk = P + static_cast<int64_t>(k) * (k + 1) / 2 * Q;
+    double ar[M], ai[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+      ar[q] = Pk[q];
+      if constexpr (CPLX) ai[q] = Pk[M + q];
+    }
+#pragma unroll 1
+    for (int i = 1; i <= k; ++i) {
+      double p[M];
+#pragma unroll
+      for (int q = 0; q < M; ++q) p[q] = Pk[i * Q + q];
+      exp_add_fast<M>(ar, p, ar, sm);
+      if constexpr (CPLX) {
+#pragma unroll
+        for (int q = 0; q < M; ++q) p[q] = Pk[i * Q + M + q];
+        exp_add_fast<M>(ai, p, ai, sm);
+      }
+    }
+    store_md<M>(Z, S, k, ar);
+    if constexpr (CPLX) store_md<M>(Z + M * S, S, k, ai);
   }
 }
 
@@ -352,6 +475,18 @@ struct Impl {
       default: k_conv<M, CPLX, 4><<<grid, kConvThreads, sh, s>>>(a); break;
     }
   }
+  static void conv_prod(const SplitArgs& a, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(a.batch) * a.njobs * a.T;
+    if (n == 0) return;
+    k_conv_prod<M, CPLX><<<static_cast<unsigned>((n + kConvThreads - 1) / kConvThreads), kConvThreads,
+                           smem(kConvThreads), s>>>(a);
+  }
+  static void conv_accum(const SplitArgs& a, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(a.batch) * a.njobs * ((a.G.d + 2) / 2);
+    if (n == 0) return;
+    k_conv_accum<M, CPLX><<<static_cast<unsigned>((n + kConvThreads - 1) / kConvThreads), kConvThreads,
+                            smem(kConvThreads), s>>>(a);
+  }
   static void add(const AddArgs& a, cudaStream_t s) {
     const int64_t n = static_cast<int64_t>(a.batch) * a.njobs * (a.G.d + 1);
     if (n == 0) return;
@@ -381,13 +516,15 @@ struct Impl {
     cudaFuncSetAttribute(k_conv<M, CPLX, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_conv<M, CPLX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_conv<M, CPLX, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
+    cudaFuncSetAttribute(k_conv_prod<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
+    cudaFuncSetAttribute(k_conv_accum<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_add<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
     cudaFuncSetAttribute(k_scale<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
     cudaFuncSetAttribute(k_extract<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
     cudaFuncSetAttribute(k_md<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
   }
   static const Launchers* table() {
-    static const Launchers L{&conv, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE};
+    static const Launchers L{&conv, &conv_prod, &conv_accum, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE};
     return &L;
   }
 };

@@ -232,15 +232,37 @@ __device__ __forceinline__ unsigned tighten_pass(double (&w)[M]) {
   return diff;
 }
 
-// Passes 1 and 2 are straight-line code (a warp almost always needs both:
-// any of its 32 lanes still changing forces another pass); later passes loop.
+// True iff a tighten pass over w would change nothing. For finite a, the pair
+// (a, b) is a fixed point of two_sum exactly when fl(a+b) == a bitwise and b
+// is not -0: then bv = a - a = +0, s - bv = a and e = +0 + b = b (which is
+// +0, not -0, when b = -0). The pairs are tested independently (one DADD
+// each, no chain), and if all are fixed points the sequential pass is a no-op.
+template <int M>
+__device__ __forceinline__ bool tighten_fixed(const double (&w)[M]) {
+  unsigned diff = 0, bad = 0;
+#pragma unroll
+  for (int i = 0; i + 1 < M; ++i) {
+    diff = diff_bits(__dadd_rn(w[i], w[i + 1]), w[i], diff);
+    const unsigned bh = static_cast<unsigned>(__double2hiint(w[i + 1]));
+    const unsigned bl = static_cast<unsigned>(__double2loint(w[i + 1]));
+    const unsigned ah = static_cast<unsigned>(__double2hiint(w[i]));
+    bad |= ((bh ^ 0x80000000u) | bl) == 0u ? 1u : 0u;            // b == -0
+    bad |= (ah & 0x7ff00000u) == 0x7ff00000u ? 1u : 0u;           // a inf/nan
+  }
+  return (diff | bad) == 0u;
+}
+
+// tighten (expansion.hpp:92-114): at most M passes, stop at the first pass
+// that changes nothing. Testing "would this pass change nothing" first
+// (tighten_fixed) replaces that final no-op pass -- 9 independent DADDs
+// instead of 9 chained two_sums -- with identical results.
 template <int M>
 __device__ __forceinline__ void tighten_fast(double (&w)[M]) {
-  if (tighten_pass<M>(w) == 0) return;
-  if (M == 2 || tighten_pass<M>(w) == 0) return;
 #pragma unroll 1
-  for (int pass = 2; pass < M; ++pass)
-    if (tighten_pass<M>(w) == 0) return;
+  for (int pass = 0; pass < M; ++pass) {
+    if (tighten_fixed<M>(w)) return;
+    tighten_pass<M>(w);
+  }
 }
 
 template <int M>
@@ -438,33 +460,26 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
       // vec_sum_err_branch over the compacted terms (popped top-down, one
       // row of look-ahead); emission jj overwrites row count-1-jj, which has
       // already been consumed
-      // Four pops per trip; each step is predicated on "still below M
-      // emissions and terms left", so a lane that finished mid-trip is inert.
       int jj = 0;
       double eps = st.s2;
-      unsigned a = st.top;               // one past the next row to pop
-      unsigned ea = st.top - kRow;       // row for emission jj
-      const unsigned bottom = ln.base;   // popping stops at row 0
+      unsigned a = st.top;
+      unsigned ea = st.top - kRow;
+      double nxt = count > 0 ? lds64(a - kRow) : 0.0;
 #pragma unroll 1
-      while (jj < M && a > bottom) {
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          v[u] = lds64(static_cast<unsigned>(max(static_cast<int>(a) - (u + 1) * static_cast<int>(kRow),
-                                                 static_cast<int>(bottom))));
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (jj < M && a > bottom) {
-            double r, tt;
-            fast_two_sum(eps, v[u], r, tt);
-            const bool emit = nonzero(tt);
-            if (emit) sts64(ea, r);
-            ea -= emit ? kRow : 0u;
-            jj += emit ? 1 : 0;
-            eps = emit ? tt : r;
-            a -= kRow;
-          }
+      for (int c = 0; c < count; ++c) {
+        const double v = nxt;
+        a -= kRow;
+        if (c + 1 < count) nxt = lds64(a - kRow);
+        double r, tt;
+        fast_two_sum(eps, v, r, tt);
+        const bool emit = nonzero(tt);
+        if (emit) {
+          sts64(ea, r);
+          ea -= kRow;
+          ++jj;
         }
+        eps = emit ? tt : r;
+        if (jj == M) break;
       }
 #pragma unroll
       for (int k = 0; k < M; ++k) {

@@ -18,6 +18,16 @@ pytestmark = pytest.mark.gpu
 LEVELS = [1, 2, 3, 4, 5, 8, 10]
 
 
+@pytest.fixture(params=["fused", "split"])
+def conv_path(request, monkeypatch):
+    """Run an engine test through the fused conv kernel (one thread per
+    coefficient pair) and through the split path (products in parallel, then
+    the accumulation chains). The planner reads PSE_SPLIT_THRESHOLD when a
+    plan is created: 0 forces fused, a huge value forces split."""
+    monkeypatch.setenv("PSE_SPLIT_THRESHOLD", "0" if request.param == "fused" else str(1 << 60))
+    return request.param
+
+
 def dev_eval(p: po.Problem, batch_stat=None):
     """evaluate() on the device for one problem; returns vg [P][m][n+1][d+1]."""
     Q = p.P * p.m
@@ -95,7 +105,7 @@ def test_series_conv_bitwise(m, cplx):
 
 
 # ---------------------------------------------------------------- whole engine
-def test_c1_bitwise_vs_reference_engine():
+def test_c1_bitwise_vs_reference_engine(conv_path):
     """C1: p1, d=15, m=2, seed 7 -- value, all 16 gradients and the whole
     dynamic arena equal run_sequential bit for bit."""
     p = po.gen_benchmark("p1", 15, 2, seed=7)
@@ -112,7 +122,7 @@ def test_c1_bitwise_vs_reference_engine():
 
 @pytest.mark.parametrize("d", [8, 31])
 @pytest.mark.parametrize("m", [1, 2, 4])
-def test_p1_bitwise_vs_sequential(d, m):
+def test_p1_bitwise_vs_sequential(d, m, conv_path):
     """acceptance criterion 6 (acceptance.cpp:163-189) with the device engine."""
     p = po.gen_benchmark("p1", d, m, seed=7)
     ref = po.evaluate(p, "port")
@@ -121,14 +131,14 @@ def test_p1_bitwise_vs_sequential(d, m):
 
 
 @pytest.mark.parametrize("pid,d,m", [("p2", 3, 2), ("p3", 3, 2), ("p2", 8, 10), ("p3", 2, 10)])
-def test_p2_p3_bitwise(pid, d, m):
+def test_p2_p3_bitwise(pid, d, m, conv_path):
     p = po.gen_benchmark(pid, d, m, seed=7)
     ref = po.evaluate(p, "port")
     vg, _ = dev_eval(p)
     assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"{pid} d={d} m={m}")
 
 
-def test_integer_instances_equal_direct_oracle():
+def test_integer_instances_equal_direct_oracle(conv_path):
     """200 positive-integer instances (half with exponents): device ==
     eval_direct bitwise (test_executor.cpp:148-159, acceptance criterion 5)."""
     rng = np.random.default_rng(506)
@@ -139,7 +149,7 @@ def test_integer_instances_equal_direct_oracle():
         assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"int instance {it}")
 
 
-def test_complex_integer_instances_equal_direct_oracle():
+def test_complex_integer_instances_equal_direct_oracle(conv_path):
     rng = np.random.default_rng(507)
     for it in range(40):
         p = int_instance(rng, False, cplx=True)
@@ -150,7 +160,7 @@ def test_complex_integer_instances_equal_direct_oracle():
 
 @pytest.mark.parametrize("m", LEVELS)
 @pytest.mark.parametrize("cplx", [False, True])
-def test_md_instances_bitwise_vs_oracle(m, cplx):
+def test_md_instances_bitwise_vs_oracle(m, cplx, conv_path):
     rng = np.random.default_rng(900 + m + 50 * cplx)
     for it in range(12):
         p = md_instance(rng, m, cplx, with_exponents=it % 3 == 0)
@@ -159,7 +169,7 @@ def test_md_instances_bitwise_vs_oracle(m, cplx):
         assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"md instance m={m} cplx={cplx} it={it}")
 
 
-def test_batched_points_equal_single_points():
+def test_batched_points_equal_single_points(conv_path):
     """one launch per layer across a batch of points == each point alone."""
     rng = np.random.default_rng(42)
     base = po.gen_benchmark("p1", 12, 4, seed=7)
