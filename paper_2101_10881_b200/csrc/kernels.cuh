@@ -295,23 +295,35 @@ __global__ void __launch_bounds__(kConvThreads) k_conv_accum(const SplitArgs a) 
   for (int c = 0; c < (k2 != k1 ? 2 : 1); ++c) {
     const int k = c ? k2 : k1;
     const double* Pk = P + static_cast<int64_t>(k) * (k + 1) / 2 * Q;
-    double ar[M], ai[M];
+    // The chain is latency-bound (one warp per scheduler at most), so the
+    // next product is fetched while the current md_add runs.
+    double ar[M], ai[M], nr[M], ni[M];
 #pragma unroll
     for (int q = 0; q < M; ++q) {
       ar[q] = Pk[q];
-      if constexpr (CPLX) ai[q] = Pk[M + q];
+      nr[q] = k >= 1 ? Pk[Q + q] : 0.0;
+      if constexpr (CPLX) {
+        ai[q] = Pk[M + q];
+        ni[q] = k >= 1 ? Pk[Q + M + q] : 0.0;
+      }
     }
 #pragma unroll 1
     for (int i = 1; i <= k; ++i) {
-      double p[M];
+      double p[M], pi[M];
 #pragma unroll
-      for (int q = 0; q < M; ++q) p[q] = Pk[i * Q + q];
-      exp_add_fast<M>(ar, p, ar, sm);
-      if constexpr (CPLX) {
-#pragma unroll
-        for (int q = 0; q < M; ++q) p[q] = Pk[i * Q + M + q];
-        exp_add_fast<M>(ai, p, ai, sm);
+      for (int q = 0; q < M; ++q) {
+        p[q] = nr[q];
+        if constexpr (CPLX) pi[q] = ni[q];
       }
+      if (i < k) {
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          nr[q] = Pk[(i + 1) * Q + q];
+          if constexpr (CPLX) ni[q] = Pk[(i + 1) * Q + M + q];
+        }
+      }
+      exp_add_fast<M, true>(ar, p, ar, sm);
+      if constexpr (CPLX) exp_add_fast<M, true>(ai, pi, ai, sm);
     }
     store_md<M>(Z, S, k, ar);
     if constexpr (CPLX) store_md<M>(Z + M * S, S, k, ai);

@@ -274,11 +274,16 @@ struct MdTraits {
   static constexpr int CAP = M == 10 ? 43 : M == 8 ? 40 : NT - 1;
   // rows per thread: CAP + one sacrificial row; the add merge reads up to row
   // 2M+1 (look-ahead past the y block)
-  static constexpr int LANE = (CAP + 1 > 2 * M + 2) ? CAP + 1 : 2 * M + 2;
+  static constexpr int LANE = (CAP + 1 > 2 * M + 3) ? CAP + 1 : 2 * M + 3;
 };
 
 // out = x + y (expansion.hpp:142-158). Safe for out aliasing x or y.
-template <int M>
+// LAT = latency-optimised merge (for latency-bound callers such as the split
+// path's accumulation chains): each side's head AND next element live in
+// registers, so the shared-memory refill is not on the compare chain. The
+// default keeps only the heads (fewer instructions, for throughput-bound
+// callers). Both produce the same merged sequence.
+template <int M, bool LAT = false>
 __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double (&y)[M], double (&out)[M], Lane ln) {
   if constexpr (M == 1) {
     out[0] = __dadd_rn(x[0], y[0]);
@@ -288,23 +293,42 @@ __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double 
       sts64(ln.base + q * kRow, x[q]);
       sts64(ln.base + (M + q) * kRow, y[q]);
     }
-    // merge by magnitude, ties take x (expansion.hpp:150-153); x and y
-    // heads live in registers, the refill comes from the lane
+    // merge by magnitude, ties take x (expansion.hpp:150-153)
     double t[2 * M];
     int i = 0;  // x elements taken; y taken = p - i
     double xh = x[0], yh = y[0];
-    unsigned xa = ln.base + kRow, ya = ln.base + (M + 1) * kRow;
+    if constexpr (!LAT) {
+      unsigned xa = ln.base + kRow, ya = ln.base + (M + 1) * kRow;
 #pragma unroll
-    for (int p = 0; p < 2 * M; ++p) {
-      const bool take_x = (p - i >= M) || (i < M && fabs(xh) >= fabs(yh));
-      t[p] = take_x ? xh : yh;
-      if (p + 1 < 2 * M) {
-        const double v = lds64(take_x ? xa : ya);
-        xh = take_x ? v : xh;
-        yh = take_x ? yh : v;
-        xa += take_x ? kRow : 0u;
-        ya += take_x ? 0u : kRow;
-        i += take_x ? 1 : 0;
+      for (int p = 0; p < 2 * M; ++p) {
+        const bool take_x = (p - i >= M) || (i < M && fabs(xh) >= fabs(yh));
+        t[p] = take_x ? xh : yh;
+        if (p + 1 < 2 * M) {
+          const double v = lds64(take_x ? xa : ya);
+          xh = take_x ? v : xh;
+          yh = take_x ? yh : v;
+          xa += take_x ? kRow : 0u;
+          ya += take_x ? 0u : kRow;
+          i += take_x ? 1 : 0;
+        }
+      }
+    } else {
+      double xn = x[1], yn = y[1];
+      unsigned xa = ln.base + 2 * kRow, ya = ln.base + (M + 2) * kRow;
+#pragma unroll
+      for (int p = 0; p < 2 * M; ++p) {
+        const bool take_x = (p - i >= M) || (i < M && fabs(xh) >= fabs(yh));
+        t[p] = take_x ? xh : yh;
+        if (p + 1 < 2 * M) {
+          const double v = lds64(take_x ? xa : ya);  // element after next
+          xh = take_x ? xn : xh;
+          yh = take_x ? yh : yn;
+          xn = take_x ? v : xn;
+          yn = take_x ? yn : v;
+          xa += take_x ? kRow : 0u;
+          ya += take_x ? 0u : kRow;
+          i += take_x ? 1 : 0;
+        }
       }
     }
     // vec_sum over 2M (expansion.hpp:61-69)
