@@ -129,9 +129,10 @@ int pse_gen_benchmark(const char* id, int32_t d, int32_t m, int32_t mode, uint64
  * for up to max_batch points on `device`. */
 int pse_plan_create(const pse_graph_desc* desc, int32_t device, int32_t max_batch, pse_plan** out);
 void pse_plan_destroy(pse_plan* p);
-/* upload `batch` points' static regions (H2D + layout transform). point_stride
- * in doubles between consecutive points inside each slab; 0 means
- * static_top*(d+1) (packed). */
+/* upload `batch` points' static regions (copy + layout transform). The slab
+ * pointers may be host memory or device memory already resident in HBM (a
+ * D2D copy then). point_stride in doubles between consecutive points inside
+ * each slab; 0 means static_top*(d+1) (packed). */
 int pse_plan_upload(pse_plan* p, int32_t batch, const double* const* static_slabs, int64_t point_stride);
 /* run all phases on the resident arena (device only); detail != 0 times every
  * phase with events, detail == 0 replays a captured CUDA graph */
@@ -144,6 +145,9 @@ int pse_plan_run(pse_plan* p, int32_t batch, const double* const* static_slabs, 
                  double* const* dyn_slabs_out, double* const* value_grad_out, pse_report* rep);
 /* plan geometry: out[8] = n, N, d, m, mode, total_slots, static_top, max_batch */
 int pse_plan_info(const pse_plan* p, int64_t* out);
+/* the plan's CUDA stream (cudaStream_t), for callers that time or order
+ * their own work against the engine's */
+int pse_plan_stream(const pse_plan* p, void** stream);
 
 /* evaluate() (executor.cpp:271-276): build graph, fold exponents (on the
  * device), stage, run, extract, for `batch` points sharing one polynomial

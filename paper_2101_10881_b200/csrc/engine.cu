@@ -518,15 +518,17 @@ void upload(Plan& p, int batch, const double* const* slabs, int64_t stride) {
   if (stride == 0) stride = pw;
   if (stride < pw) throw std::invalid_argument("point stride smaller than the static region");
   ck(cudaSetDevice(p.device), "cudaSetDevice");
+  // slabs may be host (pinned or pageable) or device pointers (UVA decides):
+  // device-resident inputs are staged with a D2D copy
   for (int q = 0; q < p.Q; ++q) {
     if (!slabs[q]) throw std::invalid_argument("null static slab");
     double* dst = p.stage + static_cast<int64_t>(q) * batch * pw;
     if (stride == pw) {
-      ck(cudaMemcpyAsync(dst, slabs[q], sizeof(double) * batch * pw, cudaMemcpyHostToDevice, p.stream), "H2D");
+      ck(cudaMemcpyAsync(dst, slabs[q], sizeof(double) * batch * pw, cudaMemcpyDefault, p.stream), "stage copy");
     } else {
       ck(cudaMemcpy2DAsync(dst, pw * sizeof(double), slabs[q], stride * sizeof(double), pw * sizeof(double), batch,
-                           cudaMemcpyHostToDevice, p.stream),
-         "H2D");
+                           cudaMemcpyDefault, p.stream),
+         "stage copy");
     }
   }
   const int64_t n = static_cast<int64_t>(p.Q) * batch * pw;
@@ -739,6 +741,12 @@ int pse_plan_run(pse_plan* p, int32_t batch, const double* const* static_slabs, 
     if (rep) *rep = r;
     return PSE_OK;
   });
+}
+
+int pse_plan_stream(const pse_plan* p, void** stream) {
+  if (!p || !stream) return PSE_EINVAL;
+  *stream = p->p->stream;
+  return PSE_OK;
 }
 
 int pse_plan_info(const pse_plan* p, int64_t* out) {

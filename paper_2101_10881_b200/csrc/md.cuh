@@ -390,8 +390,19 @@ struct Passes {
 // detected from the count and handled by the literal slow path
 template <bool CLAMP>
 __device__ __forceinline__ void push(Passes& st, double v, unsigned lim) {
-  sts64(CLAMP ? min(st.top, lim) : st.top, v);
-  st.top += nonzero(v) ? kRow : 0u;
+  // store, then advance top by one row iff v != 0 (either sign): written in
+  // PTX so ptxas emits a predicated add (STS + LOP3.P + @P IADD)
+  const unsigned addr = CLAMP ? min(st.top, lim) : st.top;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, t;\n\t"
+      "st.shared.f64 [%1], %2;\n\t"
+      "mov.b64 {lo, hi}, %2;\n\t"
+      "and.b32 t, hi, 0x7fffffff;\n\t"
+      "or.b32 t, t, lo;\n\t"
+      "setp.ne.u32 p, t, 0;\n\t"
+      "@p add.u32 %0, %0, %3;\n\t}"
+      : "+r"(st.top)
+      : "r"(addr), "d"(v), "n"(kRow));
 }
 
 // pass-1 step on term t (terms arrive t[n-2], t[n-3], ..., t[0]) followed by

@@ -403,6 +403,21 @@ class DevicePlan:
         stat, slabs = self._slabs(stat, batch)
         check(lib().pse_plan_upload(self._h, batch, slabs, 0))
 
+    def upload_ptr(self, base: int, batch: int, total: int = None, first: int = 0):
+        """Stage points [first, first+batch) of a contiguous [Q][total][top][d+1]
+        buffer at address `base` -- host or device memory (e.g. a CUDA tensor's
+        data_ptr(): inputs resident in HBM are staged with a D2D copy)."""
+        total = batch if total is None else total
+        pw = self.top * (self.graph.d + 1)
+        slabs = ptr_array([base + (q * total + first) * pw * 8 for q in range(self.Q)])
+        check(lib().pse_plan_upload(self._h, batch, slabs, 0))
+
+    def stream(self) -> int:
+        """the plan's cudaStream_t as an integer handle"""
+        s = C.c_void_p()
+        check(lib().pse_plan_stream(self._h, C.byref(s)))
+        return s.value or 0
+
     def execute(self, batch: int = 1, detail: bool = False) -> Report:
         rep = Report()
         check(lib().pse_plan_execute(self._h, batch, int(detail), C.byref(rep)))
