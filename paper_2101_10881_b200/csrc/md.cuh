@@ -30,8 +30,19 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 
 namespace pse {
+
+// compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1
+template <class F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 // ---------------------------------------------------------------- EFTs
 // two_sum: expansion.hpp:31-38 (Knuth, branch-free, 6 flops)
@@ -189,8 +200,10 @@ struct Lane {
   unsigned base;
 };
 
+// Row -1 (the first row of the allocation) is a spare: look-ahead loads may
+// touch it harmlessly.
 __device__ __forceinline__ Lane make_lane(double* smem) {
-  return Lane{static_cast<unsigned>(__cvta_generic_to_shared(smem + threadIdx.x))};
+  return Lane{static_cast<unsigned>(__cvta_generic_to_shared(smem + kLaneThreads + threadIdx.x))};
 }
 
 // volatile: the stack's stores and loads must keep their program order
@@ -200,6 +213,17 @@ __device__ __forceinline__ void sts64(unsigned addr, double v) {
 __device__ __forceinline__ double lds64(unsigned addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+// static row offsets: the offset is an immediate of the instruction
+template <unsigned OFF>
+__device__ __forceinline__ void sts64_at(unsigned base, double v) {
+  asm volatile("st.shared.f64 [%0+%2], %1;" ::"r"(base), "d"(v), "n"(OFF));
+}
+template <unsigned OFF>
+__device__ __forceinline__ double lds64_at(unsigned base) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(base), "n"(OFF));
   return v;
 }
 
@@ -239,17 +263,17 @@ __device__ __forceinline__ unsigned tighten_pass(double (&w)[M]) {
 // each, no chain), and if all are fixed points the sequential pass is a no-op.
 template <int M>
 __device__ __forceinline__ bool tighten_fixed(const double (&w)[M]) {
-  unsigned diff = 0, bad = 0;
+  unsigned diff = 0, negz = 0xffffffffu, expo = 0;
 #pragma unroll
   for (int i = 0; i + 1 < M; ++i) {
     diff = diff_bits(__dadd_rn(w[i], w[i + 1]), w[i], diff);
     const unsigned bh = static_cast<unsigned>(__double2hiint(w[i + 1]));
     const unsigned bl = static_cast<unsigned>(__double2loint(w[i + 1]));
     const unsigned ah = static_cast<unsigned>(__double2hiint(w[i]));
-    bad |= ((bh ^ 0x80000000u) | bl) == 0u ? 1u : 0u;            // b == -0
-    bad |= (ah & 0x7ff00000u) == 0x7ff00000u ? 1u : 0u;           // a inf/nan
+    negz = min(negz, (bh ^ 0x80000000u) | bl);  // 0 iff some b == -0
+    expo = max(expo, ah & 0x7ff00000u);         // 0x7ff00000 iff some a is inf/nan
   }
-  return (diff | bad) == 0u;
+  return diff == 0u && negz != 0u && expo != 0x7ff00000u;
 }
 
 // tighten (expansion.hpp:92-114): at most M passes, stop at the first pass
@@ -272,9 +296,9 @@ struct MdTraits {
   // 2e5 random full-precision pairs is 39 (M=10) and 31 (M=8), the 99th
   // percentile 31 and 24; small M reserve the full NT-1 so they never overflow.
   static constexpr int CAP = M == 10 ? 43 : M == 8 ? 40 : NT - 1;
-  // rows per thread: CAP + one sacrificial row; the add merge reads up to row
-  // 2M+1 (look-ahead past the y block)
-  static constexpr int LANE = (CAP + 1 > 2 * M + 3) ? CAP + 1 : 2 * M + 3;
+  // rows per thread: the spare row -1, then CAP + one sacrificial row; the add
+  // merge reads up to row 2M+2 (look-ahead past the y block)
+  static constexpr int LANE = 1 + ((CAP + 1 > 2 * M + 3) ? CAP + 1 : 2 * M + 3);
 };
 
 // out = x + y (expansion.hpp:142-158). Safe for out aliasing x or y.
@@ -289,10 +313,10 @@ __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double 
     out[0] = __dadd_rn(x[0], y[0]);
   } else {
 #pragma unroll
-    for (int q = 0; q < M; ++q) {
-      sts64(ln.base + q * kRow, x[q]);
-      sts64(ln.base + (M + q) * kRow, y[q]);
-    }
+    static_for<M>([&](auto q) {
+      sts64_at<decltype(q)::value * kRow>(ln.base, x[decltype(q)::value]);
+      sts64_at<(M + decltype(q)::value) * kRow>(ln.base, y[decltype(q)::value]);
+    });
     // merge by magnitude, ties take x (expansion.hpp:150-153)
     double t[2 * M];
     int i = 0;  // x elements taken; y taken = p - i
@@ -340,26 +364,28 @@ __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double 
       t[q + 1] = e;
     }
     t[0] = s;
-    // vec_sum_err_branch (expansion.hpp:74-90); emission jj goes to row jj
-    int jj = 0;
+    // vec_sum_err_branch (expansion.hpp:74-90); emission jj goes to row jj.
+    // The reference stops at the M-th emission; running on is harmless here
+    // because later emissions land in rows >= M, which are never read, and
+    // eps is only used when fewer than M were emitted -- so no per-step guard.
+    unsigned ea = ln.base;
     double eps = t[0];
 #pragma unroll
     for (int q = 1; q < 2 * M; ++q) {
-      if (jj < M) {
-        double r, tt;
-        fast_two_sum(eps, t[q], r, tt);
-        const bool emit = nonzero(tt);
-        if (emit) sts64(ln.base + jj * kRow, r);
-        jj += emit ? 1 : 0;
-        eps = emit ? tt : r;
-      }
+      double r, tt;
+      fast_two_sum(eps, t[q], r, tt);
+      const bool emit = nonzero(tt);
+      if (emit) sts64(ea, r);
+      ea += emit ? kRow : 0u;
+      eps = emit ? tt : r;
     }
-#pragma unroll
-    for (int q = 0; q < M; ++q) {
+    const int jj = static_cast<int>((ea - ln.base) / kRow);
+    static_for<M>([&](auto qc) {
+      constexpr int q = decltype(qc)::value;
       double v = 0.0;
-      if (q < jj) v = lds64(ln.base + q * kRow);
+      if (q < jj) v = lds64_at<q * kRow>(ln.base);
       out[q] = q < jj ? v : (q == jj ? eps : 0.0);
-    }
+    });
     tighten_fast<M>(out);
   }
 }
@@ -495,27 +521,26 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
       // vec_sum_err_branch over the compacted terms (popped top-down, one
       // row of look-ahead); emission jj overwrites row count-1-jj, which has
       // already been consumed
-      int jj = 0;
+      // One exit condition (terms left and fewer than M emissions), no
+      // break; the look-ahead load may read the spare row -1.
       double eps = st.s2;
-      unsigned a = st.top;
-      unsigned ea = st.top - kRow;
-      double nxt = count > 0 ? lds64(a - kRow) : 0.0;
+      unsigned a = st.top - kRow;        // row of the next term to pop
+      unsigned ea = st.top - kRow;       // row of the next emission
+      const unsigned elim = st.top - (M + 1) * kRow;  // ea == elim <=> M emitted
+      double nxt = lds64(a);
 #pragma unroll 1
-      for (int c = 0; c < count; ++c) {
+      while (a >= ln.base && ea != elim) {
         const double v = nxt;
         a -= kRow;
-        if (c + 1 < count) nxt = lds64(a - kRow);
+        nxt = lds64(a);
         double r, tt;
         fast_two_sum(eps, v, r, tt);
         const bool emit = nonzero(tt);
-        if (emit) {
-          sts64(ea, r);
-          ea -= kRow;
-          ++jj;
-        }
+        if (emit) sts64(ea, r);
+        ea -= emit ? kRow : 0u;
         eps = emit ? tt : r;
-        if (jj == M) break;
       }
+      const int jj = static_cast<int>((st.top - kRow - ea) / kRow);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
         double v = 0.0;
