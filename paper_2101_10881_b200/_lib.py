@@ -10,6 +10,8 @@ import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libpse_b200.so")
+if os.environ.get("PSE_LIB_VARIANT"):  # tuning builds (see build.py)
+    LIB_PATH = os.path.join(PKG, f"libpse_b200_{os.environ['PSE_LIB_VARIANT']}.so")
 
 PSE_MODE_REAL = 0
 PSE_MODE_COMPLEX = 1

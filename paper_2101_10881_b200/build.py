@@ -26,7 +26,13 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ARCH + [
+# tuning variants: PSE_BUILD_VARIANT=name builds libpse_b200_<name>.so from
+# objects in build_<name>/ with PSE_EXTRA_NVCC_FLAGS (e.g. -DPSE_LANE_THREADS=512)
+VARIANT = os.environ.get("PSE_BUILD_VARIANT", "")
+if VARIANT:
+    OBJ = os.path.join(PKG, "build_" + VARIANT)
+    LIB = os.path.join(PKG, f"libpse_b200_{VARIANT}.so")
+NVCC_FLAGS = os.environ.get("PSE_EXTRA_NVCC_FLAGS", "").split() + ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off",
     "-Xptxas", "-v", "-I" + INCLUDE, "-I" + CSRC,
 ]

@@ -192,7 +192,10 @@ __device__ __noinline__ void exp_mul_lit(const double* x, const double* y, doubl
 // Every kernel that uses a lane runs kLaneThreads threads per block, so the
 // row pitch is a compile-time constant and lane addresses are one 32-bit
 // shared-memory register plus an immediate offset.
-constexpr int kLaneThreads = 128;
+#ifndef PSE_LANE_THREADS
+#define PSE_LANE_THREADS 128
+#endif
+constexpr int kLaneThreads = PSE_LANE_THREADS;
 constexpr unsigned kRow = kLaneThreads * sizeof(double);  // bytes between rows
 
 // A thread's private shared-memory lane: row r at byte address base + r*kRow.
