@@ -124,6 +124,28 @@ int pse_gen_benchmark_size(const char* id, int32_t* n, int32_t* N, int32_t* shap
 int pse_gen_benchmark(const char* id, int32_t d, int32_t m, int32_t mode, uint64_t seed, int32_t* nvars,
                       int32_t* indices, double* stat);
 
+/* ---- problem files (problem_io.cpp:130-245; Problem, gen.hpp:14-19) ------- */
+/* The reference's text format: hexfloat limbs (bit-exact round trip),
+ * decimals accepted on input; parse errors return PSE_EINVAL with
+ * "line N: ..." in pse_last_error() (ParseError, problem_io.hpp:15-24). */
+typedef struct pse_problem pse_problem;
+int pse_problem_parse(const char* text, pse_problem** out);
+int pse_problem_read(const char* path, pse_problem** out);
+int pse_problem_write(const pse_problem* p, const char* path);
+/* text into buf (NUL-terminated, truncated to cap); *len = full length */
+int pse_problem_text(const pse_problem* p, char* buf, size_t cap, size_t* len);
+int pse_problem_create(const char* id, uint64_t seed, int32_t n, int32_t d, int32_t m, int32_t mode, int32_t N,
+                       const int32_t* nvars, const int32_t* indices, const int32_t* exponents, const double* stat,
+                       pse_problem** out);
+int pse_problem_gen(const char* id, int32_t d, int32_t m, int32_t mode, uint64_t seed, pse_problem** out);
+/* out[7] = n, N, d, m, mode, seed, shape length */
+int pse_problem_info(const pse_problem* p, int64_t* out);
+int pse_problem_id(const pse_problem* p, char* buf, size_t cap);
+/* arrays owned by p; exponents NULL when none; stat [Q][1+N+n][d+1] */
+int pse_problem_arrays(const pse_problem* p, const int32_t** nvars, const int32_t** indices,
+                       const int32_t** exponents, const double** stat);
+void pse_problem_destroy(pse_problem* p);
+
 /* ---- device plan -------------------------------------------------------- */
 /* Validates desc (as validate()), uploads the graph and allocates an arena
  * for up to max_batch points on `device`. */

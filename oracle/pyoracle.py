@@ -140,6 +140,10 @@ def ref_lib():
         L.ref_bench_sample.argtypes = [C.c_void_p, C.c_int, C.c_int64, _f64p]
         L.ref_run_bench.argtypes = [C.c_void_p, C.c_int, C.c_int, _f64p]
         L.ref_last_error.restype = C.c_char_p
+        L.ref_problem_to_text.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        L.ref_problem_to_text.restype = C.c_int64
+        L.ref_problem_from_text.argtypes = [C.c_char_p]
+        L.ref_problem_from_text.restype = C.c_void_p
         _ref = L
     return _ref
 
@@ -398,6 +402,44 @@ def flop_count(p: Problem, add_cost: int, mul_cost: int, which: int = 0, lib: st
         return int(L.ref_flop_count(h, d, int(p.cplx), add_cost, mul_cost, which))
     finally:
         L.ref_problem_free(h)
+
+
+def ref_problem_text(pid: str, d: int, m: int, cplx: bool = False, seed: int = 7) -> str:
+    """problem_to_text(gen_benchmark(...)) by the reference library."""
+    L = ref_lib()
+    h = L.ref_problem_gen(pid.encode(), d, m, int(cplx), seed)
+    if not h:
+        raise _err(L, "ref")
+    try:
+        n = L.ref_problem_to_text(h, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        L.ref_problem_to_text(h, buf, n + 1)
+        return buf.value.decode()
+    finally:
+        L.ref_problem_free(h)
+
+
+def ref_problem_text_of(p: Problem) -> str:
+    """problem_to_text of an arbitrary packed problem (id 'file', seed 0)."""
+    L = ref_lib()
+    h = _ref_handle(p)
+    try:
+        n = L.ref_problem_to_text(h, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        L.ref_problem_to_text(h, buf, n + 1)
+        return buf.value.decode()
+    finally:
+        L.ref_problem_free(h)
+
+
+def ref_parse_error(text: str) -> str:
+    """'' if the reference parses text, else its ParseError message."""
+    L = ref_lib()
+    h = L.ref_problem_from_text(text.encode())
+    if h:
+        L.ref_problem_free(h)
+        return ""
+    return (L.ref_last_error() or b"").decode()
 
 
 # ----------------------------------------------------------------- CPU timing

@@ -34,6 +34,7 @@
 #include "pseval/gen.hpp"
 #include "pseval/multidouble.hpp"
 #include "pseval/oracle.hpp"
+#include "pseval/problem_io.hpp"
 
 using namespace pseval;
 
@@ -386,5 +387,29 @@ int ref_run_bench(void* h, int workers, int repeats, double* out /* conv, add, w
 }
 
 int ref_hardware_threads() { return static_cast<int>(std::thread::hardware_concurrency()); }
+
+// problem_to_text (problem_io.cpp:130-157): returns the full length, copies
+// at most cap-1 bytes + NUL
+int64_t ref_problem_to_text(void* h, char* buf, int64_t cap) {
+  const std::string t = problem_to_text(static_cast<RefProblem*>(h)->p);
+  if (buf && cap > 0) {
+    const int64_t n = std::min<int64_t>(cap - 1, static_cast<int64_t>(t.size()));
+    std::memcpy(buf, t.data(), n);
+    buf[n] = 0;
+  }
+  return static_cast<int64_t>(t.size());
+}
+
+// problem_from_text (problem_io.cpp:159-245); nullptr + message on ParseError
+void* ref_problem_from_text(const char* text) {
+  try {
+    auto* r = new RefProblem;
+    r->p = problem_from_text(text);
+    return r;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
 
 }  // extern "C"

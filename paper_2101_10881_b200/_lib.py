@@ -60,6 +60,8 @@ EXPORTS = [
     "pse_plan_create", "pse_plan_destroy", "pse_plan_upload", "pse_plan_execute", "pse_plan_download",
     "pse_plan_run", "pse_plan_info", "pse_plan_stream", "pse_evaluate", "pse_md_apply", "pse_series_conv", "pse_host_alloc",
     "pse_host_free", "pse_device_info", "pse_fp64_peak",
+    "pse_problem_parse", "pse_problem_read", "pse_problem_write", "pse_problem_text", "pse_problem_create",
+    "pse_problem_gen", "pse_problem_info", "pse_problem_id", "pse_problem_arrays", "pse_problem_destroy",
 ]
 
 _lib = None
@@ -104,6 +106,17 @@ def lib():
     L.pse_host_free.argtypes = [_VP]
     L.pse_device_info.argtypes = [i32, dp]
     L.pse_fp64_peak.argtypes = [i32, dp]
+    L.pse_problem_parse.argtypes = [C.c_char_p, _PP]
+    L.pse_problem_read.argtypes = [C.c_char_p, _PP]
+    L.pse_problem_write.argtypes = [_VP, C.c_char_p]
+    L.pse_problem_text.argtypes = [_VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.pse_problem_create.argtypes = [C.c_char_p, C.c_uint64, i32, i32, i32, i32, i32, dp, dp, dp, dp, _PP]
+    L.pse_problem_gen.argtypes = [C.c_char_p, i32, i32, i32, C.c_uint64, _PP]
+    L.pse_problem_info.argtypes = [_VP, dp]
+    L.pse_problem_id.argtypes = [_VP, C.c_char_p, C.c_size_t]
+    L.pse_problem_arrays.argtypes = [_VP, C.POINTER(C.POINTER(C.c_int32)), C.POINTER(C.POINTER(C.c_int32)),
+                                     C.POINTER(C.POINTER(C.c_int32)), C.POINTER(C.POINTER(C.c_double))]
+    L.pse_problem_destroy.argtypes = [_VP]
     _lib = L
     return L
 

@@ -22,6 +22,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libpse_b200.so")
+CLI = os.path.join(PKG, "pseval_b200")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 
@@ -88,6 +89,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    # the CLI (reference tools/pseval.cpp over the device engine)
+    cli_src = os.path.join(PKG, "cli", "pseval_b200.cpp")
+    if not VARIANT and (force or not os.path.exists(CLI) or
+                        os.path.getmtime(CLI) < max(os.path.getmtime(LIB), os.path.getmtime(cli_src))):
+        cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-Wall", "-I" + INCLUDE, cli_src, "-o", CLI,
+               "-L" + PKG, "-lpse_b200", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"CLI build failed\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     return LIB
 
 

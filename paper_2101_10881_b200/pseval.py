@@ -526,6 +526,7 @@ class Problem:
     nvars: np.ndarray
     indices: np.ndarray
     stat: Optional[np.ndarray]  # [Q][1+N+n][d+1]
+    exponents: Optional[np.ndarray] = None  # [len(indices)], 0 = none for that monomial
 
     @property
     def N(self) -> int:
@@ -555,6 +556,72 @@ def gen_benchmark(pid: str, d: int, m: int, mode: str = REAL, seed: int = 7, wit
     st = np.empty((Q, 1 + N.value + n.value, d + 1), np.float64) if with_static else None
     check(lib().pse_gen_benchmark(pid.encode(), d, m, _mode_code(mode), seed, ptr(nv), ptr(ix), ptr(st)))
     return Problem(pid, seed, n.value, d, m, REAL if _mode_code(mode) == 0 else CPLX, nv, ix, st)
+
+
+# ----------------------------------------------------------------- problem files
+# problem_to_text / problem_from_text / write_problem / read_problem
+# (problem_io.hpp:26-30): hexfloat limbs, bit-exact round trip; ParseError
+# becomes InvalidArgument("line N: ...").
+def _problem_from_handle(h) -> Problem:
+    try:
+        info = np.zeros(7, np.int64)
+        check(lib().pse_problem_info(h, ptr(info)))
+        n, N, d, m, mode, seed, ln = (int(v) for v in info)
+        buf = C.create_string_buffer(256)
+        check(lib().pse_problem_id(h, buf, 256))
+        nv, ix, ex = C.POINTER(C.c_int32)(), C.POINTER(C.c_int32)(), C.POINTER(C.c_int32)()
+        st = C.POINTER(C.c_double)()
+        check(lib().pse_problem_arrays(h, C.byref(nv), C.byref(ix), C.byref(ex), C.byref(st)))
+        Q = (2 if mode else 1) * m
+        stat = np.ctypeslib.as_array(st, (Q, 1 + N + n, d + 1)).copy()
+        exps = np.ctypeslib.as_array(ex, (ln,)).copy() if ex else None
+        return Problem(buf.value.decode(), seed, n, d, m, CPLX if mode else REAL,
+                       np.ctypeslib.as_array(nv, (N,)).copy(), np.ctypeslib.as_array(ix, (ln,)).copy(), stat, exps)
+    finally:
+        lib().pse_problem_destroy(h)
+
+
+def _problem_handle(p: Problem):
+    h = C.c_void_p()
+    nv = np.ascontiguousarray(p.nvars, np.int32)
+    ix = np.ascontiguousarray(p.indices, np.int32)
+    ex = None if p.exponents is None else np.ascontiguousarray(p.exponents, np.int32)
+    st = np.ascontiguousarray(p.stat, np.float64)
+    check(lib().pse_problem_create(p.id.encode(), p.seed, p.n, p.d, p.m, _mode_code(p.mode), p.N, ptr(nv), ptr(ix),
+                                   ptr(ex), ptr(st), C.byref(h)))
+    return h
+
+
+def problem_from_text(text: str) -> Problem:
+    h = C.c_void_p()
+    check(lib().pse_problem_parse(text.encode(), C.byref(h)))
+    return _problem_from_handle(h)
+
+
+def problem_to_text(p: Problem) -> str:
+    h = _problem_handle(p)
+    try:
+        n = C.c_size_t()
+        check(lib().pse_problem_text(h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib().pse_problem_text(h, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+    finally:
+        lib().pse_problem_destroy(h)
+
+
+def read_problem(path: str) -> Problem:
+    h = C.c_void_p()
+    check(lib().pse_problem_read(path.encode(), C.byref(h)))
+    return _problem_from_handle(h)
+
+
+def write_problem(path: str, p: Problem) -> None:
+    h = _problem_handle(p)
+    try:
+        check(lib().pse_problem_write(h, path.encode()))
+    finally:
+        lib().pse_problem_destroy(h)
 
 
 # ----------------------------------------------------------------- primitives

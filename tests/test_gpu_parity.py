@@ -212,3 +212,28 @@ def test_reference_binding_drop_in():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK: 4/4" in r.stdout
+
+
+def test_cli_verify_and_bench(tmp_path):
+    """pseval_b200 verify / bench (the reference CLI's subcommands over the
+    device engine); verify cross-checks the fused and split conv paths and
+    batched against single evaluation, bit for bit."""
+    import os
+    import subprocess
+
+    cli = os.path.join(os.path.dirname(pe.LIB_PATH), "pseval_b200")
+    for args in (["verify", "p1", "--degree", "8", "--precision", "4"],
+                 ["verify", "p3", "--degree", "5", "--precision", "2", "--mode", "complex"]):
+        r = subprocess.run([cli, *args], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "verify: PASS" in r.stdout, r.stdout + r.stderr
+    path = str(tmp_path / "p2.txt")
+    assert subprocess.run([cli, "gen", "p2", path, "--degree", "3", "--precision", "3"]).returncode == 0
+    r = subprocess.run([cli, "verify", path], capture_output=True, text=True, timeout=600)
+    assert "verify: PASS" in r.stdout, r.stdout + r.stderr
+    csv = str(tmp_path / "b.csv")
+    r = subprocess.run([cli, "bench", "p1", "--degree", "8", "15", "--precision", "2", "--repeats", "2", "--csv", csv],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert "| p1 | 15 | 2 | real |" in r.stdout
+    rows = open(csv).read().strip().split("\n")
+    assert rows[0].startswith("id,d,m,mode,workers") and len(rows) == 3
