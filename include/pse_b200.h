@@ -165,6 +165,25 @@ int pse_plan_download(pse_plan* p, int32_t batch, double* const* value_grad_out,
  * contract over a DataArray (batch = 1) or a batch of points */
 int pse_plan_run(pse_plan* p, int32_t batch, const double* const* static_slabs, int64_t point_stride,
                  double* const* dyn_slabs_out, double* const* value_grad_out, pse_report* rep);
+/* ---- one polynomial sharded over devices (one plan per GPU) --------------
+ * Rank r's plan executes only the convolution jobs of its share of the
+ * independent job groups (whole monomials, contiguous and balanced by job
+ * count). The addition stage needs every term: each rank packs the dynamic
+ * slots it produced (pse_plan_pack), the blocks are exchanged (e.g. NCCL
+ * all-gather or peer copies over NVLink -- plain data movement, never an NCCL
+ * sum, which would add limbs as plain doubles), every plan unpacks the
+ * others' blocks and pse_plan_finish runs the term scales, the reference's
+ * exact addition tree and the extraction with device md_adds. The result is
+ * bit-identical to one device. pse_plan_execute on a sharded plan runs the
+ * conv stage only. Buffers are device pointers. */
+int pse_plan_create_sharded(const pse_graph_desc* desc, int32_t device, int32_t max_batch, int32_t rank,
+                            int32_t nranks, pse_plan** out);
+/* doubles in rank `rank`'s exchange block for `batch` points */
+int pse_plan_exchange_words(const pse_plan* p, int32_t rank, int32_t batch, int64_t* words);
+int pse_plan_pack(pse_plan* p, int32_t batch, double* dst);
+int pse_plan_unpack(pse_plan* p, int32_t batch, int32_t src_rank, const double* src);
+int pse_plan_finish(pse_plan* p, int32_t batch, int32_t detail, pse_report* rep);
+
 /* plan geometry: out[8] = n, N, d, m, mode, total_slots, static_top, max_batch */
 int pse_plan_info(const pse_plan* p, int64_t* out);
 /* the plan's CUDA stream (cudaStream_t), for callers that time or order

@@ -62,6 +62,7 @@ EXPORTS = [
     "pse_host_free", "pse_device_info", "pse_fp64_peak",
     "pse_problem_parse", "pse_problem_read", "pse_problem_write", "pse_problem_text", "pse_problem_create",
     "pse_problem_gen", "pse_problem_info", "pse_problem_id", "pse_problem_arrays", "pse_problem_destroy",
+    "pse_plan_create_sharded", "pse_plan_exchange_words", "pse_plan_pack", "pse_plan_unpack", "pse_plan_finish",
 ]
 
 _lib = None
@@ -117,6 +118,11 @@ def lib():
     L.pse_problem_arrays.argtypes = [_VP, C.POINTER(C.POINTER(C.c_int32)), C.POINTER(C.POINTER(C.c_int32)),
                                      C.POINTER(C.POINTER(C.c_int32)), C.POINTER(C.POINTER(C.c_double))]
     L.pse_problem_destroy.argtypes = [_VP]
+    L.pse_plan_create_sharded.argtypes = [C.POINTER(GraphDesc), i32, i32, i32, i32, _PP]
+    L.pse_plan_exchange_words.argtypes = [_VP, i32, i32, C.POINTER(i64)]
+    L.pse_plan_pack.argtypes = [_VP, i32, dp]
+    L.pse_plan_unpack.argtypes = [_VP, i32, i32, dp]
+    L.pse_plan_finish.argtypes = [_VP, i32, i32, C.POINTER(Report)]
     _lib = L
     return L
 

@@ -22,6 +22,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <set>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -80,6 +81,25 @@ __global__ void k_stage(const double* __restrict__ in, double* __restrict__ aren
     const int q = static_cast<int>(r / batch);
     arena[b * G.point_words + s * G.slot_words + static_cast<int64_t>(q) * G.S + j] =
         in[(static_cast<int64_t>(q) * batch + b) * in_point_words + s * d1 + j];
+  }
+}
+
+// exchange block of one rank: [point][i][slot_words] <-> arena slots
+template <bool PACK>
+__global__ void k_exchange(double* __restrict__ arena, double* __restrict__ buf, Geom G, const int* __restrict__ slots,
+                           int count, int batch) {
+  const int64_t n = static_cast<int64_t>(batch) * count * G.slot_words;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = t % G.slot_words;
+    const int64_t r = t / G.slot_words;
+    const int i = static_cast<int>(r % count);
+    const int64_t b = r / count;
+    double* a = arena + b * G.point_words + static_cast<int64_t>(slots[i]) * G.slot_words + w;
+    if (PACK)
+      buf[t] = *a;
+    else
+      *a = buf[t];
   }
 }
 
@@ -145,6 +165,10 @@ struct Plan {
   std::vector<ConvGroup> groups;
   cudaEvent_t fork = nullptr;
   std::vector<std::pair<int2*, int>> add_layers;
+  // sharding one polynomial over devices: this plan's rank, and per rank the
+  // dynamic slots the addition stage needs from that rank (device lists)
+  int rank = 0, nranks = 1;
+  std::vector<std::pair<int*, int>> xslots;
   int2* ts = nullptr;
   int nts = 0;
   int* row_slot = nullptr;
@@ -207,7 +231,14 @@ struct Plan {
     return 1;
   }
 
+  // whole evaluation; a sharded plan (nranks > 1) runs only its conv share
+  // here and the tail after the exchange (pse_plan_finish)
   int launch_all(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
+    const int n = launch_conv(batch, marks);
+    return nranks > 1 ? n : n + launch_tail(batch, marks);
+  }
+
+  int launch_conv(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
     int launches = 0;
     for (auto& [jobs, nj] : pro_layers) launches += launch_layer(jobs, nj, batch, groups[0], stream);
     if (groups.size() == 1) {
@@ -225,6 +256,12 @@ struct Plan {
       }
       if (marks) mark(marks, 'c');
     }
+    return launches;
+  }
+
+  // term scales, addition layers, extraction
+  int launch_tail(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
+    int launches = 0;
     if (nts) {
       ScaleArgs a{arena, G, ts, nts, batch};
       L->scale(a, stream);
@@ -260,7 +297,7 @@ struct Plan {
   }
 
   int kernel_count(int batch) const {
-    int n = (nts ? 1 : 0) + static_cast<int>(add_layers.size()) + 1;
+    int n = nranks > 1 ? 0 : (nts ? 1 : 0) + static_cast<int>(add_layers.size()) + 1;
     for (auto& [jobs, nj] : pro_layers) n += split_layer(nj, batch, groups[0]) ? 2 : 1;
     for (const ConvGroup& gr : groups)
       for (auto& [jobs, nj] : gr.layers) n += split_layer(nj, batch, gr) ? 2 : 1;
@@ -273,10 +310,11 @@ namespace {
 // Build the device plan: validate, version in-place slots, add optional
 // prologue (fold) jobs, upload job tables, allocate the arena.
 Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::vector<std::vector<ConvRow>>& prologue,
-                 int64_t prologue_slots) {
+                 int64_t prologue_slots, int rank = 0, int nranks = 1) {
   if (!valid_precision(g.m)) throw std::invalid_argument("unsupported precision level");
   if (g.mode != PSE_MODE_REAL && g.mode != PSE_MODE_COMPLEX) throw std::invalid_argument("unsupported mode");
   if (max_batch < 1) throw std::invalid_argument("max_batch must be at least 1");
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank / rank count");
   const std::string why = validate_desc(g);
   if (!why.empty()) throw std::invalid_argument("invalid job graph: " + why);
   if (g.total_slots + prologue_slots + g.conv_layer_off[g.n_conv_layers] >= (int64_t(1) << 31))
@@ -297,6 +335,8 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
   p->TS = g.total_slots;
   p->top = 1 + static_cast<int64_t>(g.N) + g.n;
   p->max_batch = max_batch;
+  p->rank = rank;
+  p->nranks = nranks;
   p->L = launchers_for(g.m, g.mode == PSE_MODE_COMPLEX);
   p->L->prepare();
 
@@ -390,21 +430,64 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
         if (!comp_jobs.count(c)) comp_order.push_back(c);
         ++comp_jobs[c];
       }
+    // Sharding one polynomial over `nranks` devices: components are dealt to
+    // ranks in contiguous ranges balanced by job count; this plan keeps only
+    // its rank's jobs (then split into concurrent groups as usual).
+    std::map<int64_t, int> comp_rank;
+    {
+      int64_t acc = 0;
+      for (int64_t c : comp_order) {
+        comp_rank[c] = static_cast<int>(std::min<int64_t>(nranks - 1, acc * nranks / std::max<int64_t>(1, njobs)));
+        acc += comp_jobs[c];
+      }
+    }
+    std::vector<int64_t> mine;
+    int64_t njobs_mine = 0;
+    for (int64_t c : comp_order)
+      if (comp_rank[c] == rank) {
+        mine.push_back(c);
+        njobs_mine += comp_jobs[c];
+      }
     const char* env = getenv("PSE_CONV_GROUPS");
     int ng = env ? atoi(env) : 4;
-    ng = std::max(1, std::min<int>(ng, static_cast<int>(comp_order.size())));
+    ng = std::max(1, std::min<int>(ng, static_cast<int>(mine.size())));
     std::map<int64_t, int> comp_group;
     int64_t acc = 0;
-    for (int64_t c : comp_order) {
-      comp_group[c] = static_cast<int>(std::min<int64_t>(ng - 1, acc * ng / std::max<int64_t>(1, njobs)));
+    for (int64_t c : mine) {
+      comp_group[c] = static_cast<int>(std::min<int64_t>(ng - 1, acc * ng / std::max<int64_t>(1, njobs_mine)));
       acc += comp_jobs[c];
     }
     p->groups.resize(ng);
     for (size_t L = npro; L < layers.size(); ++L) {
       std::vector<std::vector<ConvRow>> per(ng);
-      for (const ConvRow& r : layers[L]) per[comp_group[find(r.out)]].push_back(r);
+      for (const ConvRow& r : layers[L]) {
+        auto it = comp_group.find(find(r.out));
+        if (it != comp_group.end()) per[it->second].push_back(r);
+      }
       for (int gi = 0; gi < ng; ++gi)
         if (!per[gi].empty()) p->groups[gi].layers.push_back(upload_rows(per[gi]));
+    }
+    // exchange lists: every dynamic slot the addition stage, the term scales
+    // or the extraction reads, by the rank whose conv jobs produce it
+    if (nranks > 1) {
+      std::set<int64_t> need;
+      for (int64_t t = 0; t < g.add_layer_off[g.n_add_layers]; ++t) {
+        need.insert(g.add_src[t]);
+        need.insert(g.add_dst[t]);
+      }
+      for (int64_t t = 0; t < g.n_term_scales; ++t) need.insert(g.ts_slot[t]);
+      need.insert(g.value_slot);
+      for (int i = 0; i < g.n; ++i)
+        if (g.gradient_slots[i] >= 0) need.insert(g.gradient_slots[i]);
+      std::vector<std::vector<int>> lists(nranks);
+      for (int64_t s : need)
+        if (s >= top) lists[comp_rank[find(s)]].push_back(static_cast<int>(s));
+      p->xslots.resize(nranks);
+      for (int r2 = 0; r2 < nranks; ++r2) {
+        p->xslots[r2].second = static_cast<int>(lists[r2].size());
+        p->xslots[r2].first = lists[r2].empty() ? nullptr : dev_upload(lists[r2], s);
+        if (p->xslots[r2].first) p->owned.push_back(p->xslots[r2].first);
+      }
     }
     if (ng > 1) {
       ck(cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming), "event");
@@ -534,6 +617,54 @@ void upload(Plan& p, int batch, const double* const* slabs, int64_t stride) {
   const int64_t n = static_cast<int64_t>(p.Q) * batch * pw;
   k_stage<<<grid_for(n, 256, p.sms), 256, 0, p.stream>>>(p.stage, p.arena, p.G, p.top, batch, pw);
   ck(cudaGetLastError(), "stage launch");
+}
+
+// ---- sharding one polynomial across devices --------------------------------
+int64_t exchange_words(const Plan& p, int rank, int batch) {
+  if (p.nranks < 2) throw std::invalid_argument("plan is not sharded");
+  if (rank < 0 || rank >= p.nranks) throw std::invalid_argument("bad rank");
+  return static_cast<int64_t>(batch) * p.xslots[rank].second * p.G.slot_words;
+}
+
+// pack this rank's addition-stage slots (PACK) or write rank src's block into
+// the arena (!PACK); buf is device memory, the call is stream-ordered and
+// synchronous
+template <bool PACK>
+void exchange(Plan& p, int batch, int rank, double* buf) {
+  if (batch < 1 || batch > p.max_batch) throw std::invalid_argument("batch outside [1, max_batch]");
+  const int64_t n = exchange_words(p, rank, batch);
+  ck(cudaSetDevice(p.device), "cudaSetDevice");
+  if (n > 0) {
+    if (!buf) throw std::invalid_argument("null exchange buffer");
+    k_exchange<PACK><<<grid_for(n, 256, p.sms), 256, 0, p.stream>>>(p.arena, buf, p.G, p.xslots[rank].first,
+                                                                    p.xslots[rank].second, batch);
+    ck(cudaGetLastError(), "exchange launch");
+  }
+  ck(cudaStreamSynchronize(p.stream), "exchange");
+}
+
+// the addition stage of a sharded plan once every rank's slots are in place
+int finish(Plan& p, int batch, int detail, pse_report* rep) {
+  if (p.nranks < 2) throw std::invalid_argument("plan is not sharded");
+  if (batch < 1 || batch > p.max_batch) throw std::invalid_argument("batch outside [1, max_batch]");
+  ck(cudaSetDevice(p.device), "cudaSetDevice");
+  p.ensure_events(2);
+  (void)detail;
+  ck(cudaEventRecord(p.ev[0], p.stream), "event");
+  const int launches = p.launch_tail(batch, nullptr);
+  ck(cudaEventRecord(p.ev[1], p.stream), "event");
+  ck(cudaGetLastError(), "launch");
+  ck(cudaEventSynchronize(p.ev[1]), "finish");
+  if (rep) {
+    std::memset(rep, 0, sizeof *rep);
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, p.ev[0], p.ev[1]), "elapsed");
+    rep->wall_ms = ms;
+    rep->add_ms = ms;
+    rep->kernel_launches = launches;
+    rep->batch = batch;
+  }
+  return PSE_OK;
 }
 
 int execute(Plan& p, int batch, int detail, pse_report* rep) {
@@ -680,6 +811,49 @@ int pse_plan_create(const pse_graph_desc* desc, int32_t device, int32_t max_batc
 }
 
 void pse_plan_destroy(pse_plan* p) { delete p; }
+
+int pse_plan_create_sharded(const pse_graph_desc* desc, int32_t device, int32_t max_batch, int32_t rank,
+                            int32_t nranks, pse_plan** out) {
+  return pse::guarded([&] {
+    if (!desc || !out) throw std::invalid_argument("null argument");
+    auto* h = new pse_plan;
+    h->p.reset(pse::build_plan(*desc, device, max_batch, {}, 0, rank, nranks));
+    *out = h;
+    return PSE_OK;
+  });
+}
+
+int pse_plan_exchange_words(const pse_plan* p, int32_t rank, int32_t batch, int64_t* words) {
+  return pse::guarded([&] {
+    if (!p || !words) throw std::invalid_argument("null argument");
+    *words = pse::exchange_words(*p->p, rank, batch);
+    return PSE_OK;
+  });
+}
+
+int pse_plan_pack(pse_plan* p, int32_t batch, double* dst) {
+  return pse::guarded([&] {
+    if (!p) throw std::invalid_argument("null plan");
+    pse::exchange<true>(*p->p, batch, p->p->rank, dst);
+    return PSE_OK;
+  });
+}
+
+int pse_plan_unpack(pse_plan* p, int32_t batch, int32_t src_rank, const double* src) {
+  return pse::guarded([&] {
+    if (!p) throw std::invalid_argument("null plan");
+    if (src_rank == p->p->rank) return PSE_OK;  // own slots are already in place
+    pse::exchange<false>(*p->p, batch, src_rank, const_cast<double*>(src));
+    return PSE_OK;
+  });
+}
+
+int pse_plan_finish(pse_plan* p, int32_t batch, int32_t detail, pse_report* rep) {
+  return pse::guarded([&] {
+    if (!p) throw std::invalid_argument("null plan");
+    return pse::finish(*p->p, batch, detail, rep);
+  });
+}
 
 int pse_plan_upload(pse_plan* p, int32_t batch, const double* const* static_slabs, int64_t point_stride) {
   return pse::guarded([&] {

@@ -61,6 +61,45 @@ def sum_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
+def evaluate_sharded(plan, batch: int = 1, detail: bool = True):
+    """One evaluation of a polynomial sharded over the process group: this
+    rank's conv share, all-gather of the addition-stage term blocks (a pure
+    copy of limbs -- NCCL over NVLink on GPUs, gloo through host memory when
+    testing several ranks on one device), then the exact addition tree on
+    every rank. Returns (conv_ms, exchange_ms, finish_ms)."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    world = plan.nranks
+    dev = torch.device(f"cuda:{plan.device}")
+    words = [plan.exchange_words(r, batch) for r in range(world)]
+    width = max(1, max(words))
+    rep = plan.execute(batch, detail=detail)
+    mine = torch.zeros(width, dtype=torch.float64, device=dev)
+    t0 = time.perf_counter()
+    plan.pack(mine.data_ptr(), batch)
+    on_gpu = dist.is_initialized() and dist.get_backend() == "nccl"
+    if world == 1 or not dist.is_initialized():
+        blocks = [mine]
+    elif on_gpu:
+        blocks = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(blocks, mine)
+        torch.cuda.synchronize(dev)
+    else:
+        host = mine.cpu()
+        outs = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(outs, host)
+        blocks = [o.to(dev) for o in outs]
+    for r in range(world):
+        if r != plan.rank:
+            plan.unpack(r, blocks[r].data_ptr(), batch)
+    ex_ms = (time.perf_counter() - t0) * 1e3
+    fin = plan.finish(batch)
+    return rep.conv_ms, ex_ms, fin.wall_ms
+
+
 def gather_points(local, total: int, device=None):
     """All-gather per-rank blocks of finished series along axis 1 (points).
     local: numpy [Q][points_local][...]; returns numpy [Q][total][...].

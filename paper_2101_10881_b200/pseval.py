@@ -373,16 +373,40 @@ class DevicePlan:
     """A job graph resident on one GPU with an arena for up to max_batch
     points (pse_plan_*)."""
 
-    def __init__(self, g: JobGraph, m: int, mode: str = REAL, device: int = 0, max_batch: int = 1):
+    def __init__(self, g: JobGraph, m: int, mode: str = REAL, device: int = 0, max_batch: int = 1,
+                 rank: int = 0, nranks: int = 1):
+        """rank/nranks > 1: this plan is rank's share of one polynomial sharded
+        over nranks devices (pse_plan_create_sharded)."""
         check_precision(m)
         self.graph, self.m, self.mode, self.device, self.max_batch = g, m, mode, device, max_batch
+        self.rank, self.nranks = rank, nranks
         self.P = 2 if _mode_code(mode) else 1
         self.Q = self.P * m
         self.top = 1 + g.N + g.n
         self._desc = g.desc(m, mode)
         h = C.c_void_p()
-        check(lib().pse_plan_create(C.byref(self._desc), device, max_batch, C.byref(h)))
+        if nranks > 1:
+            check(lib().pse_plan_create_sharded(C.byref(self._desc), device, max_batch, rank, nranks, C.byref(h)))
+        else:
+            check(lib().pse_plan_create(C.byref(self._desc), device, max_batch, C.byref(h)))
         self._h = h
+
+    # ---- sharded evaluation (see include/pse_b200.h)
+    def exchange_words(self, rank: int, batch: int = 1) -> int:
+        w = C.c_int64()
+        check(lib().pse_plan_exchange_words(self._h, rank, batch, C.byref(w)))
+        return w.value
+
+    def pack(self, dst_ptr: int, batch: int = 1):
+        check(lib().pse_plan_pack(self._h, batch, dst_ptr))
+
+    def unpack(self, src_rank: int, src_ptr: int, batch: int = 1):
+        check(lib().pse_plan_unpack(self._h, batch, src_rank, src_ptr))
+
+    def finish(self, batch: int = 1, detail: bool = True) -> Report:
+        rep = Report()
+        check(lib().pse_plan_finish(self._h, batch, int(detail), C.byref(rep)))
+        return rep
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

@@ -214,6 +214,39 @@ def test_reference_binding_drop_in():
     assert "OK: 4/4" in r.stdout
 
 
+@pytest.mark.parametrize("pid,d,m,nranks", [("p1", 15, 2, 2), ("p1", 8, 4, 3), ("p3", 4, 2, 4), ("p2", 3, 3, 2)])
+def test_monomial_sharding_is_bit_exact(pid, d, m, nranks):
+    """One polynomial sharded over nranks plans (here all on device 0): each
+    runs its monomials' conv jobs, the term blocks are exchanged, each runs the
+    exact addition tree -- every rank's result equals one device's, bit for
+    bit, and the reference's."""
+    import torch
+
+    pr = pe.gen_benchmark(pid, d, m, seed=7)
+    g = pe.build_jobgraph_shape(pr.n, pr.d, pr.nvars, pr.indices)
+    full = pe.DevicePlan(g, m, "real", 0, 1)
+    ref_vg, _, _ = full.run(pr.stat, 1)
+    plans = [pe.DevicePlan(g, m, "real", 0, 1, rank=r, nranks=nranks) for r in range(nranks)]
+    width = max(1, max(plans[0].exchange_words(r) for r in range(nranks)))
+    blocks = []
+    for p in plans:
+        p.upload(pr.stat, 1)
+        p.execute(1, detail=True)
+        buf = torch.zeros(width, dtype=torch.float64, device="cuda:0")
+        p.pack(buf.data_ptr())
+        blocks.append(buf)
+    assert sum(plans[0].exchange_words(r) for r in range(nranks)) > 0
+    for p in plans:
+        for r in range(nranks):
+            p.unpack(r, blocks[r].data_ptr())
+        rep = p.finish(1)
+        assert rep.kernel_launches > 0
+        vg, _ = p.download(1)
+        assert_bitwise(vg, ref_vg, f"{pid} rank {p.rank}/{nranks}")
+    want = po.evaluate(po.gen_benchmark(pid, d, m, seed=7), "port")
+    assert_bitwise(ref_vg[:, 0].reshape(want.shape), want, "vs oracle")
+
+
 def test_cli_verify_and_bench(tmp_path):
     """pseval_b200 verify / bench (the reference CLI's subcommands over the
     device engine); verify cross-checks the fused and split conv paths and
