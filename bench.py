@@ -357,6 +357,86 @@ def ours(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def ours_sharded(args, wl):
+    """--shard monomials: ONE polynomial (C2/C4 point, seed 7) strong-scaled
+    over the ranks -- each GPU runs the conv jobs of its share of the
+    monomials, the addition-stage term slots are all-gathered over NCCL
+    (NVLink), and every rank runs the exact addition tree (bit-identical to
+    one GPU). Step time = conv (events) + exchange (host clock around
+    pack/all-gather/unpack, synchronised) + addition stage (events), max over
+    ranks."""
+    import time
+
+    import torch
+
+    import paper_2101_10881_b200 as pe
+    from paper_2101_10881_b200 import dist as D
+
+    rank, local, world = D.env_rank()
+    dev = local % max(1, torch.cuda.device_count())
+    backend = os.environ.get("PSE_DIST_BACKEND", "nccl")
+    red_dev = torch.device(f"cuda:{dev}") if backend == "nccl" else None
+    torch.cuda.set_device(dev)
+    if world > 1:
+        D.init(backend)
+    pid, d, m, _, desc = WORKLOADS[wl]
+    n, N, nvars, idx, stat = make_static(pid, d, m, range(1))
+    g = pe.build_jobgraph_shape(n, d, nvars, idx)
+    plan = pe.DevicePlan(g, m, "real", dev, 1, rank=rank, nranks=world)
+    model_ops = pe.flop_count(g, d, "real", pe.reporting_cost(m))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    pinned = torch.from_numpy(np.ascontiguousarray(stat)).pin_memory()
+
+    def step(e2e: bool):
+        t0 = time.perf_counter()
+        if e2e:
+            plan.upload_ptr(pinned.data_ptr(), 1)
+        if world > 1:
+            conv, ex, fin = D.evaluate_sharded(plan, 1)
+        else:
+            r = plan.execute(1, detail=True)
+            conv, ex, fin = r.conv_ms, 0.0, r.wall_ms - r.conv_ms
+        if e2e and rank == 0:
+            plan.download(1)
+        return conv + ex + fin, conv, (time.perf_counter() - t0) * 1e3
+
+    plan.upload(stat, 1)
+    for _ in range(args.warmup):
+        step(False)
+    if world > 1:
+        torch.distributed.barrier()
+    walls, convs, e2es = [], [], []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            flush.random_(0, 255)
+            torch.cuda.synchronize(dev)
+            w, c, _ = step(False)
+            walls.append(w)
+            convs.append(c)
+    for _ in range(args.steps):
+        e2es.append(step(True)[2])
+    total = D.max_over_ranks(sum(walls), red_dev)
+    e2e_total = D.max_over_ranks(sum(e2es), red_dev)
+    if rank != 0:
+        return
+    ms = total / args.steps
+    line = {
+        "metric": METRIC, "value": model_ops / (ms * 1e-3) / 1e12, "unit": "TFLOPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "ms_per_eval": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (gen_benchmark seed 7)",
+        "config": {"workload": desc + " -- one polynomial sharded by monomials", "id": pid, "d": d, "m": m,
+                   "points": 1, "parallelism": f"monomials x{world} (exact addition tree after an all-gather)",
+                   "l2": "256 MiB buffer rewritten between timed steps"},
+        "conv_ms_rank0": sum(convs) / args.steps,
+        "e2e": {"value": model_ops / (e2e_total / args.steps * 1e-3) / 1e12, "unit": "TFLOPS",
+                "ms_per_call": e2e_total / args.steps, "timing": "host clock, synchronised",
+                "h2d_bytes_per_step": int(stat.nbytes), "d2h_bytes_per_step": int(plan.Q * (n + 1) * (d + 1) * 8)},
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -365,6 +445,9 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--wave", type=int, default=128, help="points per device launch (C5)")
+    ap.add_argument("--shard", default="points", choices=["points", "monomials"],
+                    help="points: each rank evaluates its own points (weak scaling, default); monomials: one "
+                         "polynomial split over the ranks (strong scaling, exact)")
     ap.add_argument("--points", type=int, default=0,
                     help="override the workload's point count (per GPU for C1-C4, total for C5)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -373,6 +456,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         reference_arm(args, args.workload)
+    elif args.shard == "monomials":
+        ours_sharded(args, args.workload)
     else:
         ours(args, args.workload)
 
