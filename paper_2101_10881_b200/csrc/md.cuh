@@ -219,11 +219,11 @@ __device__ __forceinline__ double lds64(unsigned addr) {
   return v;
 }
 // static row offsets: the offset is an immediate of the instruction
-template <unsigned OFF>
+template <int OFF>
 __device__ __forceinline__ void sts64_at(unsigned base, double v) {
   asm volatile("st.shared.f64 [%0+%2], %1;" ::"r"(base), "d"(v), "n"(OFF));
 }
-template <unsigned OFF>
+template <int OFF>
 __device__ __forceinline__ double lds64_at(unsigned base) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(base), "n"(OFF));
@@ -233,6 +233,28 @@ __device__ __forceinline__ double lds64_at(unsigned base) {
 // v != 0.0 (either sign) on the integer pipe: one LOP3 + one ISETP
 __device__ __forceinline__ bool nonzero(double v) {
   return ((static_cast<unsigned>(__double2hiint(v)) & 0x7fffffffu) | static_cast<unsigned>(__double2loint(v))) != 0u;
+}
+
+// One vec_sum_err_branch step (expansion.hpp:80-87) against a shared-memory
+// emission row: (r, tt) = fast_two_sum(eps, v); if tt != 0 (either sign) r is
+// stored at row ea, ea moves one row (down when DOWN) and eps = tt, otherwise
+// eps = r. In PTX so the store, the row advance and the eps select all hang
+// off one predicate (LOP3.P, @P STS, @P IADD, 2 SEL).
+template <bool DOWN>
+__device__ __forceinline__ void emit_step(double& eps, double v, unsigned& ea) {
+  double r, tt;
+  fast_two_sum(eps, v, r, tt);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, t;\n\t"
+      "mov.b64 {lo, hi}, %3;\n\t"
+      "and.b32 t, hi, 0x7fffffff;\n\t"
+      "or.b32 t, t, lo;\n\t"
+      "setp.ne.u32 p, t, 0;\n\t"
+      "@p st.shared.f64 [%1], %2;\n\t"
+      "@p add.u32 %1, %1, %4;\n\t"
+      "selp.f64 %0, %3, %2, p;\n\t}"
+      : "=d"(eps), "+r"(ea)
+      : "d"(r), "d"(tt), "n"(DOWN ? 0u - kRow : kRow));
 }
 
 // bitwise inequality accumulator: d |= bits(a) ^ bits(b)
@@ -374,14 +396,7 @@ __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double 
     unsigned ea = ln.base;
     double eps = t[0];
 #pragma unroll
-    for (int q = 1; q < 2 * M; ++q) {
-      double r, tt;
-      fast_two_sum(eps, t[q], r, tt);
-      const bool emit = nonzero(tt);
-      if (emit) sts64(ea, r);
-      ea += emit ? kRow : 0u;
-      eps = emit ? tt : r;
-    }
+    for (int q = 1; q < 2 * M; ++q) emit_step<false>(eps, t[q], ea);
     const int jj = static_cast<int>((ea - ln.base) / kRow);
     static_for<M>([&](auto qc) {
       constexpr int q = decltype(qc)::value;
@@ -524,24 +539,23 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
       // vec_sum_err_branch over the compacted terms (popped top-down, one
       // row of look-ahead); emission jj overwrites row count-1-jj, which has
       // already been consumed
-      // One exit condition (terms left and fewer than M emissions), no
-      // break; the look-ahead load may read the spare row -1.
+      // Continue while terms are left and fewer than M were emitted; two
+      // pops per trip with a test between them (no register rotation). The
+      // look-ahead load may read the spare row -1, never below.
       double eps = st.s2;
       unsigned a = st.top - kRow;        // row of the next term to pop
       unsigned ea = st.top - kRow;       // row of the next emission
       const unsigned elim = st.top - (M + 1) * kRow;  // ea == elim <=> M emitted
-      double nxt = lds64(a);
+      const unsigned base1 = ln.base + kRow;
+      double n0 = lds64(a);
 #pragma unroll 1
       while (a >= ln.base && ea != elim) {
-        const double v = nxt;
-        a -= kRow;
-        nxt = lds64(a);
-        double r, tt;
-        fast_two_sum(eps, v, r, tt);
-        const bool emit = nonzero(tt);
-        if (emit) sts64(ea, r);
-        ea -= emit ? kRow : 0u;
-        eps = emit ? tt : r;
+        const double n1 = lds64_at<-static_cast<int>(kRow)>(a);  // row a-1 >= spare row
+        emit_step<true>(eps, n0, ea);
+        if (a < base1 || ea == elim) break;
+        n0 = lds64_at<-2 * static_cast<int>(kRow)>(a);  // row a-2 >= spare row (a-1 >= base)
+        emit_step<true>(eps, n1, ea);
+        a -= 2 * kRow;
       }
       const int jj = static_cast<int>((st.top - kRow - ea) / kRow);
 #pragma unroll
