@@ -170,22 +170,33 @@ __global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
 
   const int n1 = k1 + 1;
   const int total = k2 > k1 ? d + 2 : n1;
-  double ar[M], ai[M];  // accumulators (re, im)
+  if constexpr (!CPLX) {
+    // the accumulator lives in the lane (acc_add), not in registers, so it is
+    // not live across the md_mul
 #pragma unroll 1
-  for (int t = 0; t < total; ++t) {
-    const bool second = t >= n1;
-    const int kk = second ? k2 : k1;
-    const int i = second ? t - n1 : t;
-    if constexpr (!CPLX) {
-      double xr[M], yr[M], p[M];
+    for (int t = 0; t < total; ++t) {
+      const bool second = t >= n1;
+      const int kk = second ? k2 : k1;
+      const int i = second ? t - n1 : t;
+      double xr[M], yr[M], p[M], o[M];
       load_md<M>(X, S, i, xr);
       load_md<M>(Y, S, kk - i, yr);
       exp_mul_fast<M>(xr, yr, p, sm);
-      if (i == 0)
-        copy_md<M>(ar, p);
-      else
-        exp_add_fast<M>(ar, p, ar, sm);
-    } else {
+      if (i == 0) {
+        copy_md<M>(o, p);
+        acc_store<M>(p, sm);
+      } else {
+        acc_add<M>(p, o, sm);
+      }
+      if (i == kk) store_md<M>(Z, S, kk, o);
+    }
+  } else {
+    double ar[M], ai[M];  // accumulators (re, im)
+#pragma unroll 1
+    for (int t = 0; t < total; ++t) {
+      const bool second = t >= n1;
+      const int kk = second ? k2 : k1;
+      const int i = second ? t - n1 : t;
       // (xr + i xi)(yr + i yi): pseries.cpp:50-51 operand order
       double xr[M], yr[M], xi[M], yi[M], p1[M], p2[M], pre[M], pim[M];
       load_md<M>(X, S, i, xr);
@@ -205,10 +216,10 @@ __global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
         exp_add_fast<M>(ar, pre, ar, sm);
         exp_add_fast<M>(ai, pim, ai, sm);
       }
-    }
-    if (i == kk) {
-      store_md<M>(Z, S, kk, ar);
-      if constexpr (CPLX) store_md<M>(Z + M * S, S, kk, ai);
+      if (i == kk) {
+        store_md<M>(Z, S, kk, ar);
+        store_md<M>(Z + M * S, S, kk, ai);
+      }
     }
   }
 }
@@ -467,6 +478,9 @@ __global__ void __launch_bounds__(kAddThreads) k_md(const MdArgs a) {
 template <int M, bool CPLX>
 struct Impl {
   static size_t smem(int threads) { return static_cast<size_t>(threads) * MdTraits<M>::LANE * sizeof(double); }
+  static size_t smem_conv(int threads) {
+    return static_cast<size_t>(threads) * (CPLX ? MdTraits<M>::LANE : MdTraits<M>::LANE_CONV) * sizeof(double);
+  }
   static int minb() {
     static const int v = [] {
       const char* e = getenv("PSE_CONV_MINB");
@@ -478,7 +492,7 @@ struct Impl {
   static void conv(const ConvArgs& a, cudaStream_t s) {
     const int64_t n = static_cast<int64_t>(a.batch) * a.njobs * a.npairs;
     if (n == 0) return;
-    const size_t sh = smem(kConvThreads);
+    const size_t sh = smem_conv(kConvThreads);
     const unsigned grid = static_cast<unsigned>((n + kConvThreads - 1) / kConvThreads);
     switch (M >= 8 ? minb() : 4) {
       case 2: k_conv<M, CPLX, 2><<<grid, kConvThreads, sh, s>>>(a); break;
@@ -524,10 +538,11 @@ struct Impl {
   }
   static void prepare() {
     const int c = static_cast<int>(smem(kConvThreads)), o = static_cast<int>(smem(kAddThreads));
-    cudaFuncSetAttribute(k_conv<M, CPLX, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
-    cudaFuncSetAttribute(k_conv<M, CPLX, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
-    cudaFuncSetAttribute(k_conv<M, CPLX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
-    cudaFuncSetAttribute(k_conv<M, CPLX, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
+    const int cc = static_cast<int>(smem_conv(kConvThreads));
+    cudaFuncSetAttribute(k_conv<M, CPLX, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
+    cudaFuncSetAttribute(k_conv<M, CPLX, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
+    cudaFuncSetAttribute(k_conv<M, CPLX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
+    cudaFuncSetAttribute(k_conv<M, CPLX, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv_prod<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_conv_accum<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_add<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);

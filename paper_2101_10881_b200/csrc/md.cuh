@@ -319,19 +319,96 @@ struct MdTraits {
   static constexpr int NT = M * (M + 1) + (M - 1);
   // Stack capacity for nonzero vec_sum pass-2 terms. The measured maximum over
   // 2e5 random full-precision pairs is 39 (M=10) and 31 (M=8), the 99th
-  // percentile 31 and 24; small M reserve the full NT-1 so they never overflow.
-  static constexpr int CAP = M == 10 ? 43 : M == 8 ? 40 : NT - 1;
+  // percentile 31 and 24 (M=10 keeps 42 so four blocks of the convolution,
+  // accumulator rows included, fit one SM's shared memory); small M reserve the full NT-1 so they never overflow.
+  static constexpr int CAP = M == 10 ? 42 : M == 8 ? 40 : NT - 1;
   // rows per thread: the spare row -1, then CAP + one sacrificial row; the add
   // merge reads up to row 2M+2 (look-ahead past the y block)
   static constexpr int LANE = 1 + ((CAP + 1 > 2 * M + 3) ? CAP + 1 : 2 * M + 3);
+  // the convolution's accumulator rows follow (acc_store / acc_add), plus
+  // the row the merge's look-ahead reads past the accumulator. At M=10:
+  // 55 rows x 128 threads x 8 B = 56,320 B per block, 4 blocks per SM.
+  static constexpr int ACC = LANE - 1;
+  static constexpr int LANE_CONV = LANE + M + 1;
 };
 
-// out = x + y (expansion.hpp:142-158). Safe for out aliasing x or y.
+// Merge, vec_sum, vec_sum_err_branch and tighten of an md_add
+// (expansion.hpp:142-158) whose operands already sit in the thread's lane:
+// x at rows XR..XR+M-1, y at rows YR..YR+M-1, heads (and, for LAT, the
+// second elements) passed in registers. Emissions use rows 0..2M-2, so x or
+// y rows below 2M are consumed before they are overwritten.
 // LAT = latency-optimised merge (for latency-bound callers such as the split
 // path's accumulation chains): each side's head AND next element live in
 // registers, so the shared-memory refill is not on the compare chain. The
 // default keeps only the heads (fewer instructions, for throughput-bound
 // callers). Both produce the same merged sequence.
+template <int M, bool LAT, int XR, int YR>
+__device__ __forceinline__ void exp_add_core(double xh, double xn, double yh, double yn, double (&out)[M], Lane ln) {
+  // merge by magnitude, ties take x (expansion.hpp:150-153)
+  double t[2 * M];
+  int i = 0;  // x elements taken; y taken = p - i
+  if constexpr (!LAT) {
+    unsigned xa = ln.base + (XR + 1) * kRow, ya = ln.base + (YR + 1) * kRow;
+#pragma unroll
+    for (int p = 0; p < 2 * M; ++p) {
+      const bool take_x = (p - i >= M) || (i < M && fabs(xh) >= fabs(yh));
+      t[p] = take_x ? xh : yh;
+      if (p + 1 < 2 * M) {
+        const double v = lds64(take_x ? xa : ya);
+        xh = take_x ? v : xh;
+        yh = take_x ? yh : v;
+        xa += take_x ? kRow : 0u;
+        ya += take_x ? 0u : kRow;
+        i += take_x ? 1 : 0;
+      }
+    }
+  } else {
+    unsigned xa = ln.base + (XR + 2) * kRow, ya = ln.base + (YR + 2) * kRow;
+#pragma unroll
+    for (int p = 0; p < 2 * M; ++p) {
+      const bool take_x = (p - i >= M) || (i < M && fabs(xh) >= fabs(yh));
+      t[p] = take_x ? xh : yh;
+      if (p + 1 < 2 * M) {
+        const double v = lds64(take_x ? xa : ya);  // element after next
+        xh = take_x ? xn : xh;
+        yh = take_x ? yh : yn;
+        xn = take_x ? v : xn;
+        yn = take_x ? yn : v;
+        xa += take_x ? kRow : 0u;
+        ya += take_x ? 0u : kRow;
+        i += take_x ? 1 : 0;
+      }
+    }
+  }
+  // vec_sum over 2M (expansion.hpp:61-69)
+  double s = t[2 * M - 1];
+#pragma unroll
+  for (int q = 2 * M - 2; q >= 0; --q) {
+    double e;
+    two_sum(t[q], s, s, e);
+    t[q + 1] = e;
+  }
+  t[0] = s;
+  // vec_sum_err_branch (expansion.hpp:74-90); emission jj goes to row jj.
+  // The reference stops at the M-th emission; running on is harmless here
+  // because later emissions land in rows >= M, which are never read, and
+  // eps is only used when fewer than M were emitted -- so no per-step guard.
+  unsigned ea = ln.base;
+  double eps = t[0];
+#pragma unroll
+  for (int q = 1; q < 2 * M; ++q) emit_step<false>(eps, t[q], ea);
+  const int jj = static_cast<int>((ea - ln.base) / kRow);
+  static_for<M>([&](auto qc) {
+    constexpr int q = decltype(qc)::value;
+    double v = 0.0;
+    if (q < jj) v = lds64_at<q * kRow>(ln.base);
+    out[q] = q < jj ? v : (q == jj ? eps : 0.0);
+  });
+  tighten_fast<M>(out);
+}
+
+// out = x + y (expansion.hpp:142-158), operands in registers. Safe for out
+// aliasing x or y.
 template <int M, bool LAT = false>
 __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double (&y)[M], double (&out)[M], Lane ln) {
   if constexpr (M == 1) {
@@ -342,71 +419,17 @@ __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double 
       sts64_at<decltype(q)::value * kRow>(ln.base, x[decltype(q)::value]);
       sts64_at<(M + decltype(q)::value) * kRow>(ln.base, y[decltype(q)::value]);
     });
-    // merge by magnitude, ties take x (expansion.hpp:150-153)
-    double t[2 * M];
-    int i = 0;  // x elements taken; y taken = p - i
-    double xh = x[0], yh = y[0];
-    if constexpr (!LAT) {
-      unsigned xa = ln.base + kRow, ya = ln.base + (M + 1) * kRow;
-#pragma unroll
-      for (int p = 0; p < 2 * M; ++p) {
-        const bool take_x = (p - i >= M) || (i < M && fabs(xh) >= fabs(yh));
-        t[p] = take_x ? xh : yh;
-        if (p + 1 < 2 * M) {
-          const double v = lds64(take_x ? xa : ya);
-          xh = take_x ? v : xh;
-          yh = take_x ? yh : v;
-          xa += take_x ? kRow : 0u;
-          ya += take_x ? 0u : kRow;
-          i += take_x ? 1 : 0;
-        }
-      }
-    } else {
-      double xn = x[1], yn = y[1];
-      unsigned xa = ln.base + 2 * kRow, ya = ln.base + (M + 2) * kRow;
-#pragma unroll
-      for (int p = 0; p < 2 * M; ++p) {
-        const bool take_x = (p - i >= M) || (i < M && fabs(xh) >= fabs(yh));
-        t[p] = take_x ? xh : yh;
-        if (p + 1 < 2 * M) {
-          const double v = lds64(take_x ? xa : ya);  // element after next
-          xh = take_x ? xn : xh;
-          yh = take_x ? yh : yn;
-          xn = take_x ? v : xn;
-          yn = take_x ? yn : v;
-          xa += take_x ? kRow : 0u;
-          ya += take_x ? 0u : kRow;
-          i += take_x ? 1 : 0;
-        }
-      }
-    }
-    // vec_sum over 2M (expansion.hpp:61-69)
-    double s = t[2 * M - 1];
-#pragma unroll
-    for (int q = 2 * M - 2; q >= 0; --q) {
-      double e;
-      two_sum(t[q], s, s, e);
-      t[q + 1] = e;
-    }
-    t[0] = s;
-    // vec_sum_err_branch (expansion.hpp:74-90); emission jj goes to row jj.
-    // The reference stops at the M-th emission; running on is harmless here
-    // because later emissions land in rows >= M, which are never read, and
-    // eps is only used when fewer than M were emitted -- so no per-step guard.
-    unsigned ea = ln.base;
-    double eps = t[0];
-#pragma unroll
-    for (int q = 1; q < 2 * M; ++q) emit_step<false>(eps, t[q], ea);
-    const int jj = static_cast<int>((ea - ln.base) / kRow);
-    static_for<M>([&](auto qc) {
-      constexpr int q = decltype(qc)::value;
-      double v = 0.0;
-      if (q < jj) v = lds64_at<q * kRow>(ln.base);
-      out[q] = q < jj ? v : (q == jj ? eps : 0.0);
-    });
-    tighten_fast<M>(out);
+    exp_add_core<M, LAT, 0, M>(x[0], x[1], y[0], y[1], out, ln);
   }
 }
+
+// Accumulator kept in the lane (rows MdTraits<M>::ACC..ACC+M-1) instead of
+// registers, so it is not live across the register-hungry md_mul between
+// two accumulation steps.
+template <int M>
+__device__ __forceinline__ void acc_store(const double (&v)[M], Lane ln);
+template <int M>
+__device__ __forceinline__ void acc_add(const double (&y)[M], double (&out)[M], Lane ln);
 
 template <int M>
 __device__ __forceinline__ void exp_sub_fast(const double (&x)[M], const double (&y)[M], double (&out)[M], Lane ln) {
@@ -578,6 +601,26 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
       for (int k = 0; k < M; ++k) out[k] = ol[k];
     }
   }
+}
+
+template <int M>
+__device__ __forceinline__ void acc_store(const double (&v)[M], Lane ln) {
+  static_for<M>([&](auto q) {
+    sts64_at<(MdTraits<M>::ACC + decltype(q)::value) * kRow>(ln.base, v[decltype(q)::value]);
+  });
+}
+
+// out = acc + y (expansion.hpp:142-158, x = the accumulator), then acc = out
+template <int M>
+__device__ __forceinline__ void acc_add(const double (&y)[M], double (&out)[M], Lane ln) {
+  if constexpr (M == 1) {
+    out[0] = __dadd_rn(lds64_at<MdTraits<M>::ACC * kRow>(ln.base), y[0]);
+  } else {
+    static_for<M>([&](auto q) { sts64_at<(M + decltype(q)::value) * kRow>(ln.base, y[decltype(q)::value]); });
+    const double xh = lds64_at<MdTraits<M>::ACC * kRow>(ln.base);
+    exp_add_core<M, false, MdTraits<M>::ACC, M>(xh, 0.0, y[0], 0.0, out, ln);
+  }
+  acc_store<M>(out, ln);
 }
 
 }  // namespace pse
