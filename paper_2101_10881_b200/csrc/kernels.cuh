@@ -103,10 +103,16 @@ struct Launchers {
 constexpr int kConvThreads = kLaneThreads;
 constexpr int kAddThreads = kLaneThreads;
 
+// limb q of coefficient j at src[q*S + j]: one pointer walked by S (a 64-bit
+// add per limb instead of re-deriving every address from the indices)
 template <int M>
 __device__ __forceinline__ void load_md(const double* __restrict__ src, int S, int j, double (&v)[M]) {
+  const double* p = src + j;
 #pragma unroll
-  for (int q = 0; q < M; ++q) v[q] = src[q * S + j];
+  for (int q = 0; q < M; ++q) {
+    v[q] = __ldg(p);
+    p += S;
+  }
 }
 
 template <int M>

@@ -230,6 +230,20 @@ __device__ __forceinline__ double lds64_at(unsigned base) {
   return v;
 }
 
+// v = (lim >= THR) ? word at base+OFF : +0.0 -- predicated load, no selects
+template <int OFF, unsigned THR>
+__device__ __forceinline__ double lds64_at_if(unsigned base, unsigned lim) {
+  double v;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ge.u32 p, %2, %3;\n\t"
+      "mov.b64 %0, 0;\n\t"
+      "@p ld.shared.f64 %0, [%1+%4];\n\t}"
+      : "=d"(v)
+      : "r"(base), "r"(lim), "n"(THR), "n"(OFF));
+  return v;
+}
+
 // v != 0.0 (either sign) on the integer pipe: one LOP3 + one ISETP
 __device__ __forceinline__ bool nonzero(double v) {
   return ((static_cast<unsigned>(__double2hiint(v)) & 0x7fffffffu) | static_cast<unsigned>(__double2loint(v))) != 0u;
@@ -286,19 +300,27 @@ __device__ __forceinline__ unsigned tighten_pass(double (&w)[M]) {
 // is not -0: then bv = a - a = +0, s - bv = a and e = +0 + b = b (which is
 // +0, not -0, when b = -0). The pairs are tested independently (one DADD
 // each, no chain), and if all are fixed points the sequential pass is a no-op.
+//
+// Precondition (holds for every caller: tighten runs on the output of
+// vec_sum_err_branch, and on its own output): no w[i], i >= 1, is -0.
+//  * two_sum's error e = (a - av) + (b - bv) is never -0: both terms would
+//    have to be -0, i.e. a = b = -0 and av = bv = +0, but then
+//    av = s - bv = -0. So vec_sum tails and tighten's w[i+1] are never -0.
+//  * err_branch emits r only when t != 0, and then r != 0; the final eps sits
+//    at position >= 1 only after a step with a term that is nonzero (popped
+//    stack terms) or not -0 (vec_sum tails), after which fl(eps + v) is not
+//    -0. Padding is +0.
+// So the "b is not -0" half of the test is vacuous here. Non-finite values:
+// if w[0] is finite and some later w[i] is not, the first pair (finite a,
+// non-finite b) has fl(a+b) non-finite != a and is caught by the bit test;
+// so checking w[0] alone for inf/nan completes the test.
 template <int M>
 __device__ __forceinline__ bool tighten_fixed(const double (&w)[M]) {
-  unsigned diff = 0, negz = 0xffffffffu, expo = 0;
+  unsigned diff = 0;
 #pragma unroll
-  for (int i = 0; i + 1 < M; ++i) {
-    diff = diff_bits(__dadd_rn(w[i], w[i + 1]), w[i], diff);
-    const unsigned bh = static_cast<unsigned>(__double2hiint(w[i + 1]));
-    const unsigned bl = static_cast<unsigned>(__double2loint(w[i + 1]));
-    const unsigned ah = static_cast<unsigned>(__double2hiint(w[i]));
-    negz = min(negz, (bh ^ 0x80000000u) | bl);  // 0 iff some b == -0
-    expo = max(expo, ah & 0x7ff00000u);         // 0x7ff00000 iff some a is inf/nan
-  }
-  return diff == 0u && negz != 0u && expo != 0x7ff00000u;
+  for (int i = 0; i + 1 < M; ++i) diff = diff_bits(__dadd_rn(w[i], w[i + 1]), w[i], diff);
+  const unsigned ah = static_cast<unsigned>(__double2hiint(w[0]));
+  return diff == 0u && (ah & 0x7ff00000u) != 0x7ff00000u;
 }
 
 // tighten (expansion.hpp:92-114): at most M passes, stop at the first pass
@@ -397,12 +419,13 @@ __device__ __forceinline__ void exp_add_core(double xh, double xn, double yh, do
   double eps = t[0];
 #pragma unroll
   for (int q = 1; q < 2 * M; ++q) emit_step<false>(eps, t[q], ea);
-  const int jj = static_cast<int>((ea - ln.base) / kRow);
+  // rows 0..jj-1 hold the emissions; eps goes to row jj (when jj >= M it is
+  // never read) and rows beyond jj read as zero
+  sts64(ea, eps);
+  const unsigned jb = ea - ln.base;
   static_for<M>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
-    double v = 0.0;
-    if (q < jj) v = lds64_at<q * kRow>(ln.base);
-    out[q] = q < jj ? v : (q == jj ? eps : 0.0);
+    out[q] = lds64_at_if<q * kRow, q * kRow>(ln.base, jb);
   });
   tighten_fast<M>(out);
 }
@@ -580,13 +603,14 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
         emit_step<true>(eps, n1, ea);
         a -= 2 * kRow;
       }
-      const int jj = static_cast<int>((st.top - kRow - ea) / kRow);
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        double v = 0.0;
-        if (k < jj) v = lds64(st.top - (k + 1) * kRow);
-        out[k] = k < jj ? v : (k == jj ? eps : 0.0);
-      }
+      // emission k sits at row top-1-k; eps goes to the next emission row
+      // (rows below the stack are never reached: ea >= top-(M+1) rows >= -1)
+      sts64(ea, eps);
+      const unsigned jb = st.top - kRow - ea;  // jj rows, in bytes
+      static_for<M>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        out[k] = lds64_at_if<-(k + 1) * static_cast<int>(kRow), k * kRow>(st.top, jb);
+      });
       tighten_fast<M>(out);
     } else {
       // rare: more nonzero terms than the lane holds -> literal algorithm
