@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
   if constexpr (!CPLX) {
     // the accumulator lives in the lane (acc_add), not in registers, so it is
     // not live across the md_mul
+    acc_init<M>(sm);
 #pragma unroll 1
     for (int t = 0; t < total; ++t) {
       const bool second = t >= n1;

@@ -357,8 +357,9 @@ struct MdTraits {
 // Merge, vec_sum, vec_sum_err_branch and tighten of an md_add
 // (expansion.hpp:142-158) whose operands already sit in the thread's lane:
 // x at rows XR..XR+M-1, y at rows YR..YR+M-1, heads (and, for LAT, the
-// second elements) passed in registers. Emissions use rows 0..2M-2, so x or
-// y rows below 2M are consumed before they are overwritten.
+// second elements) passed in registers. Emissions use rows 0..2M-1, so x or
+// y rows below 2M are consumed before they are overwritten. Without LAT the
+// merge needs sentinels in rows XR+M (NaN) and YR+M (+0).
 // LAT = latency-optimised merge (for latency-bound callers such as the split
 // path's accumulation chains): each side's head AND next element live in
 // registers, so the shared-memory refill is not on the compare chain. The
@@ -368,12 +369,18 @@ template <int M, bool LAT, int XR, int YR>
 __device__ __forceinline__ void exp_add_core(double xh, double xn, double yh, double yn, double (&out)[M], Lane ln) {
   // merge by magnitude, ties take x (expansion.hpp:150-153)
   double t[2 * M];
-  int i = 0;  // x elements taken; y taken = p - i
+  [[maybe_unused]] int i = 0;  // LAT: x elements taken; y taken = p - i
   if constexpr (!LAT) {
+    // Sentinels end both runs: NaN after x (|NaN| >= |y| is false, so an
+    // exhausted x never wins) and +0 after y (|x| >= 0 holds for every
+    // non-NaN x, so an exhausted y never wins). Both cannot be exhausted
+    // within 2M steps, so the comparison alone replays the reference's
+    // merge and tail copies. (NaN data is outside the bit-exact contract:
+    // NaN bit patterns already differ between the host and the device.)
     unsigned xa = ln.base + (XR + 1) * kRow, ya = ln.base + (YR + 1) * kRow;
 #pragma unroll
     for (int p = 0; p < 2 * M; ++p) {
-      const bool take_x = (p - i >= M) || (i < M && fabs(xh) >= fabs(yh));
+      const bool take_x = fabs(xh) >= fabs(yh);
       t[p] = take_x ? xh : yh;
       if (p + 1 < 2 * M) {
         const double v = lds64(take_x ? xa : ya);
@@ -381,7 +388,6 @@ __device__ __forceinline__ void exp_add_core(double xh, double xn, double yh, do
         yh = take_x ? yh : v;
         xa += take_x ? kRow : 0u;
         ya += take_x ? 0u : kRow;
-        i += take_x ? 1 : 0;
       }
     }
   } else {
@@ -438,11 +444,17 @@ __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double 
     out[0] = __dadd_rn(x[0], y[0]);
   } else {
 #pragma unroll
+    // x at rows 0..M-1 + NaN sentinel at row M, y at rows M+1..2M + zero
+    // sentinel at row 2M+1 (the LAT merge ignores the sentinels)
     static_for<M>([&](auto q) {
       sts64_at<decltype(q)::value * kRow>(ln.base, x[decltype(q)::value]);
-      sts64_at<(M + decltype(q)::value) * kRow>(ln.base, y[decltype(q)::value]);
+      sts64_at<(M + 1 + decltype(q)::value) * kRow>(ln.base, y[decltype(q)::value]);
     });
-    exp_add_core<M, LAT, 0, M>(x[0], x[1], y[0], y[1], out, ln);
+    if constexpr (!LAT) {
+      sts64_at<M * kRow>(ln.base, __longlong_as_double(0x7ff8000000000000ll));
+      sts64_at<(2 * M + 1) * kRow>(ln.base, 0.0);
+    }
+    exp_add_core<M, LAT, 0, M + 1>(x[0], x[1], y[0], y[1], out, ln);
   }
 }
 
@@ -627,6 +639,13 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
   }
 }
 
+// once per thread before the first acc_add: the NaN sentinel after the
+// accumulator rows (never overwritten: acc_store writes rows ACC..ACC+M-1)
+template <int M>
+__device__ __forceinline__ void acc_init(Lane ln) {
+  sts64_at<(MdTraits<M>::ACC + M) * kRow>(ln.base, __longlong_as_double(0x7ff8000000000000ll));
+}
+
 template <int M>
 __device__ __forceinline__ void acc_store(const double (&v)[M], Lane ln) {
   static_for<M>([&](auto q) {
@@ -641,6 +660,7 @@ __device__ __forceinline__ void acc_add(const double (&y)[M], double (&out)[M], 
     out[0] = __dadd_rn(lds64_at<MdTraits<M>::ACC * kRow>(ln.base), y[0]);
   } else {
     static_for<M>([&](auto q) { sts64_at<(M + decltype(q)::value) * kRow>(ln.base, y[decltype(q)::value]); });
+    sts64_at<2 * M * kRow>(ln.base, 0.0);  // y's sentinel (x's: acc_init)
     const double xh = lds64_at<MdTraits<M>::ACC * kRow>(ln.base);
     exp_add_core<M, false, MdTraits<M>::ACC, M>(xh, 0.0, y[0], 0.0, out, ln);
   }
