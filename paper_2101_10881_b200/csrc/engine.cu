@@ -24,6 +24,7 @@
 #include <map>
 #include <set>
 #include <memory>
+#include <queue>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -139,6 +140,225 @@ T* dev_upload(const std::vector<T>& v, cudaStream_t s) {
   return p;
 }
 
+// Banded conv schedule (see BandArgs in kernels.cuh). Tasks (job, band b,
+// segment s <= b) -- one per band for copy jobs -- with the dependencies:
+//   (J, b, s-1)                   the running sum of the same chains;
+//   final band s of in1's job     steps i in segment s read x_i, i in band s;
+//   final bands <= b of in2's job (segment 0; later segments read less);
+// where "final band b" of a job is its task (b, b) (copy: its band-b task).
+// Static inputs and prologue outputs are ready before the first wave. Tasks
+// are list-scheduled into waves of at most `cap2` half-warps (a rectangular
+// or copy task fills a warp, a diagonal task half of one), highest
+// longest-path-to-exit first; each wave becomes one launch (banded mode), or
+// the waves, flattened, are the order in which the dataflow kernel hands out
+// descriptors (flow mode; the per-descriptor dependency lists serve it).
+struct BandSched {
+  std::vector<std::vector<int4>> waves;  // warp descriptors per wave
+  std::vector<int> dep_off, deps;        // per descriptor (numbered in wave order): descriptors it waits for
+};
+
+BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int64_t cap2, bool flow, int64_t procs, double slack) {
+  const int nb = 1 + d / kBandW;  // band 0 = [0, d % W + 1), then full bands (kernels.cuh)
+  const int W0 = d % kBandW + 1;
+  auto lo = [&](int b) { return b == 0 ? 0 : W0 + (b - 1) * kBandW; };
+  const int nj = static_cast<int>(rows.size());
+  std::map<int64_t, int> producer;
+  for (int j = 0; j < nj; ++j) producer[rows[j].out] = j;
+  std::vector<int64_t> base(nj + 1, 0);
+  for (int j = 0; j < nj; ++j) base[j + 1] = base[j] + (rows[j].copy ? nb : nb * (nb + 1) / 2);
+  const int64_t T = base[nj];
+  auto fin = [&](int j, int b) { return rows[j].copy ? base[j] + b : base[j] + b * (b + 1) / 2 + b; };
+  std::vector<int> tjob(T);
+  std::vector<int16_t> tb(T), ts(T);  // ts = -1: copy task
+  std::vector<std::pair<int64_t, int64_t>> edges;
+  for (int j = 0; j < nj; ++j) {
+    const auto px = producer.find(rows[j].in1);
+    const int X = px == producer.end() ? -1 : px->second;
+    int Y = -1;
+    if (!rows[j].copy) {
+      const auto py = producer.find(rows[j].in2);
+      Y = py == producer.end() ? -1 : py->second;
+    }
+    if (X >= j || Y >= j) throw std::logic_error("band schedule: jobs not in dependency order");
+    for (int b = 0; b < nb; ++b) {
+      if (rows[j].copy) {
+        const int64_t t = base[j] + b;
+        tjob[t] = j, tb[t] = b, ts[t] = -1;
+        if (X >= 0) edges.emplace_back(fin(X, b), t);
+        continue;
+      }
+      for (int s2 = 0; s2 <= b; ++s2) {
+        const int64_t t = base[j] + b * (b + 1) / 2 + s2;
+        tjob[t] = j, tb[t] = b, ts[t] = s2;
+        if (s2 > 0) edges.emplace_back(t - 1, t);
+        if (X >= 0) edges.emplace_back(fin(X, s2), t);
+        if (s2 == 0 && Y >= 0)
+          for (int b2 = 0; b2 <= b; ++b2) edges.emplace_back(fin(Y, b2), t);
+      }
+    }
+  }
+  // successor lists (CSR); every edge goes from a lower to a higher task id
+  std::vector<int64_t> off(T + 1, 0), succ(edges.size());
+  std::vector<int> indeg(T, 0);
+  for (auto& e : edges) ++off[e.first + 1], ++indeg[e.second];
+  for (int64_t t = 0; t < T; ++t) off[t + 1] += off[t];
+  {
+    std::vector<int64_t> fill(off.begin(), off.end() - 1);
+    for (auto& e : edges) succ[fill[e.first]++] = e.second;
+  }
+  std::vector<int> prio(T, 1);
+  for (int64_t t = T - 1; t >= 0; --t)
+    for (int64_t e = off[t]; e < off[t + 1]; ++e) prio[t] = std::max(prio[t], prio[succ[e]] + 1);
+  // predecessor lists (descriptor dependencies, pairing checks)
+  std::vector<int64_t> poff(T + 1, 0), pred(edges.size());
+  for (auto& e : edges) ++poff[e.second + 1];
+  for (int64_t t = 0; t < T; ++t) poff[t + 1] += poff[t];
+  {
+    std::vector<int64_t> fill(poff.begin(), poff.end() - 1);
+    for (auto& e : edges) pred[fill[e.second]++] = e.first;
+  }
+  auto is_diag = [&](int64_t t) { return ts[t] >= 0 && ts[t] == tb[t]; };
+  BandSched out;
+  std::vector<int> desc_of(T, -1);
+  std::vector<std::pair<int64_t, int64_t>> members;  // tasks of each descriptor (second = -1: none)
+  auto desc_for = [&](int64_t t, int64_t t2) {
+    const int j = tjob[t], b = tb[t], s2 = ts[t];
+    if (s2 < 0) return make_int4(j, lo(b), 0, -3);
+    if (s2 < b) return make_int4(j, lo(b), lo(s2), -1);
+    return make_int4(j, lo(b), lo(b), t2 >= 0 ? tjob[t2] : -2);
+  };
+  auto add_desc = [&](std::vector<int4>& w, int64_t t1, int64_t t2) {
+    desc_of[t1] = static_cast<int>(members.size());
+    if (t2 >= 0) desc_of[t2] = static_cast<int>(members.size());
+    members.emplace_back(t1, t2);
+    w.push_back(desc_for(t1, t2));
+  };
+  if (flow) {
+    // Greedy list scheduling simulated in time on `procs` warps (a task
+    // lasts its steps / kBandW; a diagonal task, half a warp, half that);
+    // a task becomes ready `slack` after its last dependency finishes, so
+    // in the resulting hand-out order a unit's dependencies are, where the
+    // graph allows, a little more than one round of warps earlier.
+    std::vector<int> indeg2 = indeg;
+    std::vector<double> rt(T, 0.0);
+    using Ev = std::pair<double, int64_t>;
+    std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> pending;  // (ready time, task)
+    std::priority_queue<std::pair<int, int64_t>> ready;                   // (prio, -task)
+    std::priority_queue<double, std::vector<double>, std::greater<double>> procfree;
+    for (int64_t q = 0; q < std::max<int64_t>(1, procs); ++q) procfree.push(0.0);
+    for (int64_t t = 0; t < T; ++t)
+      if (indeg2[t] == 0) pending.emplace(0.0, t);
+    std::vector<int64_t> order;
+    order.reserve(T);
+    while (static_cast<int64_t>(order.size()) < T) {
+      double now = procfree.top();
+      while (!pending.empty() && pending.top().first <= now) {
+        ready.emplace(prio[pending.top().second], -pending.top().second);
+        pending.pop();
+      }
+      if (ready.empty()) {
+        if (pending.empty()) throw std::logic_error("band schedule: dependency cycle");
+        procfree.pop();
+        procfree.push(pending.top().first);
+        continue;
+      }
+      const int64_t t = -ready.top().second;
+      ready.pop();
+      procfree.pop();
+      const int wb = tb[t] == 0 ? W0 : kBandW, wsg = ts[t] == 0 ? W0 : kBandW;
+      const double dur = ts[t] < 0 ? 0.1 : is_diag(t) ? (wb + 1) / (2.0 * kBandW) : double(wsg) / kBandW;
+      const double fin = now + dur;
+      procfree.push(fin);
+      order.push_back(t);
+      for (int64_t e = off[t]; e < off[t + 1]; ++e) {
+        const int64_t u = succ[e];
+        rt[u] = std::max(rt[u], fin + slack);
+        if (--indeg2[u] == 0) pending.emplace(rt[u], u);
+      }
+    }
+    // descriptors in that order; a diagonal task joins the last open
+    // diagonal descriptor of its band (at most 64 descriptors back) when
+    // all its dependencies precede that descriptor
+    std::vector<int4> w;
+    std::map<int, int> open;  // band -> descriptor with a free half
+    for (int64_t t : order) {
+      if (!is_diag(t)) {
+        add_desc(w, t, -1);
+        continue;
+      }
+      const auto it = open.find(tb[t]);
+      bool joined = false;
+      if (it != open.end() && static_cast<int>(members.size()) - it->second <= 64) {
+        int latest = -1;
+        for (int64_t e = poff[t]; e < poff[t + 1]; ++e) latest = std::max(latest, desc_of[pred[e]]);
+        if (latest < it->second) {
+          members[it->second].second = t;
+          desc_of[t] = it->second;
+          w[it->second].w = tjob[t];
+          open.erase(it);
+          joined = true;
+        }
+      }
+      if (!joined) {
+        open[tb[t]] = static_cast<int>(members.size());
+        add_desc(w, t, -1);
+      }
+    }
+    out.waves.push_back(std::move(w));
+  } else {
+    auto cost = [&](int64_t t) { return is_diag(t) ? 1 : 2; };
+    std::vector<int> indeg2 = indeg;
+    std::priority_queue<std::pair<int, int64_t>> ready;  // (prio, -id)
+    for (int64_t t = 0; t < T; ++t)
+      if (indeg2[t] == 0) ready.emplace(prio[t], -t);
+    int64_t done = 0;
+    while (done < T) {
+      if (ready.empty()) throw std::logic_error("band schedule: dependency cycle");
+      std::vector<int64_t> picked;
+      int64_t used = 0;
+      while (!ready.empty() && used + cost(-ready.top().second) <= std::max<int64_t>(cap2, 2)) {
+        const int64_t t = -ready.top().second;
+        ready.pop();
+        used += cost(t);
+        picked.push_back(t);
+      }
+      std::vector<int4> w;
+      std::map<int, std::vector<int64_t>> diag;  // band -> tasks
+      for (int64_t t : picked) {
+        if (is_diag(t))
+          diag[tb[t]].push_back(t);
+        else
+          add_desc(w, t, -1);
+      }
+      for (auto& [b, ts2] : diag)
+        for (size_t q = 0; q < ts2.size(); q += 2) add_desc(w, ts2[q], q + 1 < ts2.size() ? ts2[q + 1] : -1);
+      out.waves.push_back(std::move(w));
+      for (int64_t t : picked)
+        for (int64_t e = off[t]; e < off[t + 1]; ++e)
+          if (--indeg2[succ[e]] == 0) ready.emplace(prio[succ[e]], -succ[e]);
+      done += static_cast<int64_t>(picked.size());
+    }
+  }
+  // descriptor dependency lists
+  out.dep_off.assign(1, 0);
+  for (size_t dsc = 0; dsc < members.size(); ++dsc) {
+    std::vector<int> ds;
+    for (int64_t t : {members[dsc].first, members[dsc].second}) {
+      if (t < 0) continue;
+      for (int64_t e = poff[t]; e < poff[t + 1]; ++e) {
+        const int q = desc_of[pred[e]];
+        if (q >= static_cast<int>(dsc)) throw std::logic_error("band schedule: dependency not scheduled earlier");
+        ds.push_back(q);
+      }
+    }
+    std::sort(ds.begin(), ds.end());
+    ds.erase(std::unique(ds.begin(), ds.end()), ds.end());
+    out.deps.insert(out.deps.end(), ds.begin(), ds.end());
+    out.dep_off.push_back(static_cast<int>(out.deps.size()));
+  }
+  return out;
+}
+
 }  // namespace
 
 struct Plan {
@@ -188,10 +408,76 @@ struct Plan {
   int64_t flops_model = 0, alg_ops = 0, conv_jobs = 0, add_jobs = 0, copy_jobs = 0;
   std::map<int, cudaGraphExec_t> graphs;
   std::vector<cudaEvent_t> ev;
+  // Banded conv stage (deep graphs with few jobs per layer, see BandArgs):
+  // this rank's non-prologue conv jobs in layer order, their device table,
+  // and per batch size the task waves (one launch each).
+  std::vector<ConvRow> band_rows;
+  int4* band_jobs = nullptr;
+  struct BandWaves {
+    int4* tasks = nullptr;
+    std::vector<std::pair<int64_t, int>> waves;  // (offset, warps)
+    int* dep_off = nullptr;  // flow mode
+    int* deps = nullptr;
+    int nunits = 0;
+  };
+  unsigned* flow_flags = nullptr;  // [max_batch][units] (grown on demand)
+  int64_t flow_flag_words = 0;
+  unsigned long long* flow_counter = nullptr;
+  std::map<int, BandWaves> band_waves;
+  int conv_mode = 0;         // PSE_CONV_MODE: 0 auto, 1 layered, 2 banded waves, 3 dataflow
+  double band_rounds = 1.0;  // PSE_BAND_ROUNDS: wave size in resident warps
+  double flow_slack = 0.3;   // PSE_FLOW_SLACK: see band_schedule
+  int64_t layer_pairs = 0;   // average conv layer size in coefficient pairs
+
+  // Layered when the average conv layer offers at least two waves of
+  // resident threads (one per coefficient pair), banded otherwise.
+  bool banded(int batch) const {
+    if (band_rows.empty() || conv_mode == 1) return false;
+    if (conv_mode >= 2) return true;
+    return static_cast<int64_t>(batch) * layer_pairs < int64_t(sms) * 4 * 128 * 2;
+  }
+
+  bool flow() const { return conv_mode == 3 || conv_mode == 0; }
+
+  // host schedule + upload for a batch size (never during stream capture)
+  void prepare_band(int batch) {
+    if (!banded(batch) || band_waves.count(batch)) return;
+    const int warps = sms * L->band_blocks_per_sm() * (kLaneThreads / 32);
+    const int64_t cap2 = std::max<int64_t>(2, static_cast<int64_t>(2 * band_rounds * warps / batch));
+    const BandSched sch = band_schedule(band_rows, d, cap2, flow(), std::max(1, warps / batch), flow_slack);
+    std::vector<int4> all;
+    BandWaves bw;
+    for (auto& w : sch.waves) {
+      bw.waves.emplace_back(static_cast<int64_t>(all.size()), static_cast<int>(w.size()));
+      all.insert(all.end(), w.begin(), w.end());
+    }
+    bw.tasks = dev_upload(all, stream);
+    bw.nunits = static_cast<int>(all.size());
+    if (flow()) {
+      bw.dep_off = dev_upload(sch.dep_off, stream);
+      bw.deps = dev_upload(sch.deps, stream);
+      const int64_t need = static_cast<int64_t>(batch) * bw.nunits;
+      if (need > flow_flag_words) {
+        cudaFree(flow_flags);
+        flow_flags = dev_alloc<unsigned>(static_cast<size_t>(need));
+        flow_flag_words = need;
+      }
+      if (!flow_counter) flow_counter = dev_alloc<unsigned long long>(1);
+    }
+    ck(cudaStreamSynchronize(stream), "band upload");
+    band_waves.emplace(batch, std::move(bw));
+  }
 
   ~Plan() {
     if (device >= 0) cudaSetDevice(device);
     for (auto& [b, g] : graphs) cudaGraphExecDestroy(g);
+    for (auto& [b, w] : band_waves) {
+      cudaFree(w.tasks);
+      cudaFree(w.dep_off);
+      cudaFree(w.deps);
+    }
+    cudaFree(flow_flags);
+    cudaFree(flow_counter);
     for (cudaEvent_t x : ev) cudaEventDestroy(x);
     for (void* p : owned) cudaFree(p);
     cudaFree(arena);
@@ -241,7 +527,23 @@ struct Plan {
   int launch_conv(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
     int launches = 0;
     for (auto& [jobs, nj] : pro_layers) launches += launch_layer(jobs, nj, batch, groups[0], stream);
-    if (groups.size() == 1) {
+    if (banded(batch)) {
+      const BandWaves& bw = band_waves.at(batch);
+      if (flow()) {
+        ck(cudaMemsetAsync(flow_flags, 0, sizeof(unsigned) * batch * bw.nunits, stream), "flags");
+        ck(cudaMemsetAsync(flow_counter, 0, sizeof(unsigned long long), stream), "counter");
+        FlowArgs a{arena, G, band_jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, flow_flags, flow_counter};
+        L->conv_flow(a, sms * L->band_blocks_per_sm(), stream);
+        ++launches;
+      } else {
+        for (auto& [o, nw] : bw.waves) {
+          BandArgs a{arena, G, band_jobs, bw.tasks + o, nw, batch};
+          L->conv_band(a, stream);
+          ++launches;
+        }
+      }
+      if (marks) mark(marks, 'c');
+    } else if (groups.size() == 1) {
       for (auto& [jobs, nj] : groups[0].layers) {
         launches += launch_layer(jobs, nj, batch, groups[0], stream);
         if (marks) mark(marks, 'c');
@@ -299,6 +601,7 @@ struct Plan {
   int kernel_count(int batch) const {
     int n = nranks > 1 ? 0 : (nts ? 1 : 0) + static_cast<int>(add_layers.size()) + 1;
     for (auto& [jobs, nj] : pro_layers) n += split_layer(nj, batch, groups[0]) ? 2 : 1;
+    if (banded(batch)) return n + (flow() ? 1 : static_cast<int>(band_waves.at(batch).waves.size()));
     for (const ConvGroup& gr : groups)
       for (auto& [jobs, nj] : gr.layers) n += split_layer(nj, batch, gr) ? 2 : 1;
     return n;
@@ -458,14 +761,37 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
       acc += comp_jobs[c];
     }
     p->groups.resize(ng);
+    int64_t nlayers = 0;
     for (size_t L = npro; L < layers.size(); ++L) {
       std::vector<std::vector<ConvRow>> per(ng);
       for (const ConvRow& r : layers[L]) {
         auto it = comp_group.find(find(r.out));
-        if (it != comp_group.end()) per[it->second].push_back(r);
+        if (it != comp_group.end()) {
+          per[it->second].push_back(r);
+          p->band_rows.push_back(r);
+        }
       }
+      if (!layers[L].empty()) ++nlayers;
       for (int gi = 0; gi < ng; ++gi)
         if (!per[gi].empty()) p->groups[gi].layers.push_back(upload_rows(per[gi]));
+    }
+    p->layer_pairs = static_cast<int64_t>(p->band_rows.size()) * ((g.d + 2) / 2) / std::max<int64_t>(1, nlayers);
+    if (!p->band_rows.empty()) {
+      std::vector<int4> v;
+      for (auto& r : p->band_rows)
+        v.push_back(make_int4(static_cast<int>(r.in1), static_cast<int>(r.in2), static_cast<int>(r.out),
+                              (r.in1 >= top ? 2 : 0) | (!r.copy && r.in2 >= top ? 4 : 0)));
+      p->band_jobs = dev_upload(v, s);
+      p->owned.push_back(p->band_jobs);
+    }
+    {
+      const char* cm = getenv("PSE_CONV_MODE");
+      const std::string m = cm ? cm : "";
+      p->conv_mode = m == "layer" ? 1 : m == "band" ? 2 : m == "flow" ? 3 : 0;
+      const char* br = getenv("PSE_BAND_ROUNDS");
+      if (br && atof(br) > 0) p->band_rounds = atof(br);
+      const char* fs = getenv("PSE_FLOW_SLACK");
+      if (fs && atof(fs) >= 0) p->flow_slack = atof(fs);
     }
     // exchange lists: every dynamic slot the addition stage, the term scales
     // or the extraction reads, by the rank whose conv jobs produce it
@@ -671,6 +997,7 @@ int execute(Plan& p, int batch, int detail, pse_report* rep) {
   if (batch < 1 || batch > p.max_batch) throw std::invalid_argument("batch outside [1, max_batch]");
   ck(cudaSetDevice(p.device), "cudaSetDevice");
   p.ensure_events(2);
+  p.prepare_band(batch);
   int launches = 0;
   if (detail) {
     std::vector<std::pair<char, cudaEvent_t>> marks;

@@ -86,8 +86,56 @@ struct SplitArgs {
   int T;
 };
 
+// Banded convolution (deep graphs, few jobs per layer). A conv job's output
+// coefficients are cut into bands -- band 0 = [0, W0) with W0 = d % kBandW + 1,
+// then full bands of kBandW, so that every rectangular task fills a warp --
+// and the accumulation chain of a coefficient k (steps i = 0..k, ascending)
+// into segments at the same boundaries.
+// A task (job, band b, segment s <= b) runs the steps i in segment s of the
+// chains of every k in band b; the running sum is carried between segments
+// in the output slot itself (exact binary64 words), so the operation order of
+// conv() is unchanged and the result is bit-identical. A task needs only
+// band s of in1 and bands <= b-s of in2, so a job's low bands finish -- and
+// unlock the next layer -- while its high bands still accumulate: the host
+// schedules tasks into waves (one launch each) over that dependency graph.
+// One warp per task descriptor (int4 {job, k0, i0, aux}):
+//   aux == -1  rectangular task (s < b): lane l owns k = k0 + l, the steps
+//              i of segment s (all < k0 <= k);
+//   aux >= 0 or -2  diagonal tasks (s == b) of two jobs (x = job, aux =
+//              second job or -2 for none), one per half-warp: lane j owns
+//              k = k0+j and k = k0+width-1-j, steps k0..k -- width+1 steps
+//              per lane, balanced;
+//   aux == -3  copy job, band k0: out := in1 on coefficients k0 + lane.
+constexpr int kBandW = 32;
+
+struct BandArgs {
+  double* arena;
+  Geom G;
+  const int4* jobs;   // (in1, in2, out, flags) of every banded conv job;
+                      // flags: 2 = in1 and 4 = in2 produced by a conv job
+  const int4* tasks;  // warp descriptors of one wave
+  int ntasks;
+  int batch;
+};
+
+struct FlowArgs {
+  double* arena;
+  Geom G;
+  const int4* jobs;     // as BandArgs
+  const int4* tasks;    // every descriptor, in scheduled order
+  const int* dep_off;   // [nunits+1] CSR of the descriptors each one waits for
+  const int* deps;
+  int nunits;
+  int batch;
+  unsigned* flags;      // [batch][nunits], zero before the launch
+  unsigned long long* counter;  // zero before the launch
+};
+
 struct Launchers {
   void (*conv)(const ConvArgs&, cudaStream_t);
+  void (*conv_band)(const BandArgs&, cudaStream_t);
+  void (*conv_flow)(const FlowArgs&, int blocks, cudaStream_t);
+  int (*band_blocks_per_sm)();
   void (*conv_prod)(const SplitArgs&, cudaStream_t);
   void (*conv_accum)(const SplitArgs&, cudaStream_t);
   void (*add)(const AddArgs&, cudaStream_t);
@@ -111,6 +159,18 @@ __device__ __forceinline__ void load_md(const double* __restrict__ src, int S, i
 #pragma unroll
   for (int q = 0; q < M; ++q) {
     v[q] = __ldg(p);
+    p += S;
+  }
+}
+
+// coh: the series may be written during this kernel by other SMs, so it is
+// read through L2 (ld.global.cg) instead of the non-coherent read-only path
+template <int M>
+__device__ __forceinline__ void load_md_sel(const double* __restrict__ src, int S, int j, double (&v)[M], bool coh) {
+  const double* p = src + j;
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    v[q] = coh ? __ldcg(p) : __ldg(p);
     p += S;
   }
 }
@@ -228,6 +288,178 @@ __global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
         store_md<M>(Z + M * S, S, kk, ai);
       }
     }
+  }
+}
+
+// ------------------------------------------------- banded convolution (deep)
+// See BandArgs. Every lane runs at most two chain pieces (kA: steps
+// iaA..ibA, then kB: steps iaB..ibB) through ONE loop body, like k_conv's
+// coefficient pair. A piece that starts past i = 0 resumes from the partial
+// sum its job's previous segment stored in Z[k]; every piece ends by storing
+// its sum there (final once i reaches k).
+// COH (dataflow kernel): inputs produced by conv jobs (flag bits 1 and 2 of
+// the job's .w) may have been written during this kernel by other SMs and
+// are read through L2; static inputs keep the read-only path.
+template <int M, bool CPLX, bool COH>
+__device__ __forceinline__ void band_task(double* arena, const Geom& G, const int4* __restrict__ jobs, const int4 T,
+                                          int64_t pt, int lane, Lane sm) {
+  const int S = G.S, d = G.d;
+  constexpr int Q = CPLX ? 2 * M : M;
+  double* base = arena + pt * G.point_words;
+  // band 0 is [0, W0) with W0 = d % kBandW + 1, the others are full
+  const int W0 = d % kBandW + 1;
+  const int width = T.y == 0 ? W0 : kBandW;
+  int job = T.x, kA, iaA, ibA, kB = -1, iaB = 0, ibB = -1;
+  if (T.w == -1 || T.w == -3) {
+    if (lane >= width) return;
+    kA = T.y + lane;
+    iaA = T.z;
+    ibA = (T.z == 0 ? W0 : T.z + kBandW) - 1;
+  } else {
+    if (lane >= 16) job = T.w;
+    const int j = lane & 15;
+    if (2 * j >= width) return;
+    kA = T.y + j;
+    iaA = T.y;
+    ibA = kA;
+    kB = T.y + width - 1 - j;
+    iaB = T.y;
+    ibB = kB;
+    if (kB == kA) kB = -1;
+  }
+  if (job < 0 || kA > d) return;
+  const int4 J = jobs[job];
+  const double* __restrict__ X = base + static_cast<int64_t>(J.x) * G.slot_words;
+  const double* __restrict__ Y = base + static_cast<int64_t>(J.y) * G.slot_words;
+  double* Z = base + static_cast<int64_t>(J.z) * G.slot_words;
+  const bool cx = COH && (J.w & 2), cy = COH && (J.w & 4);
+  if (T.w == -3) {  // copy job (executor.cpp:130-133)
+#pragma unroll 1
+    for (int q = 0; q < Q; ++q) Z[q * S + kA] = cx ? __ldcg(X + q * S + kA) : X[q * S + kA];
+    return;
+  }
+  const int nA = ibA - iaA + 1;
+  const int total = nA + (kB >= 0 ? ibB - iaB + 1 : 0);
+  if constexpr (!CPLX) {
+    acc_init<M>(sm);
+    double o[M];
+#pragma unroll 1
+    for (int t = 0; t < total; ++t) {
+      const bool second = t >= nA;
+      const int k = second ? kB : kA;
+      const int ia = second ? iaB : iaA;
+      const int i = second ? iaB + (t - nA) : iaA + t;
+      double xr[M], yr[M], p[M];
+      load_md_sel<M>(X, S, i, xr, cx);
+      load_md_sel<M>(Y, S, k - i, yr, cy);
+      exp_mul_fast<M>(xr, yr, p, sm);
+      if (i == 0) {
+        copy_md<M>(o, p);
+        acc_store<M>(p, sm);
+      } else {
+        if (i == ia) {  // resume the partial sum of the previous segment
+#pragma unroll
+          for (int q = 0; q < M; ++q) o[q] = __ldcg(Z + q * S + k);
+          acc_store<M>(o, sm);
+        }
+        acc_add<M>(p, o, sm);
+      }
+      if (i == (second ? ibB : ibA)) store_md<M>(Z, S, k, o);
+    }
+  } else {
+    double ar[M], ai[M];
+#pragma unroll 1
+    for (int t = 0; t < total; ++t) {
+      const bool second = t >= nA;
+      const int k = second ? kB : kA;
+      const int ia = second ? iaB : iaA;
+      const int i = second ? iaB + (t - nA) : iaA + t;
+      double xr[M], yr[M], xi[M], yi[M], p1[M], p2[M], pre[M], pim[M];
+      load_md_sel<M>(X, S, i, xr, cx);
+      load_md_sel<M>(Y, S, k - i, yr, cy);
+      load_md_sel<M>(X + M * S, S, i, xi, cx);
+      load_md_sel<M>(Y + M * S, S, k - i, yi, cy);
+      exp_mul_fast<M>(xr, yr, p1, sm);
+      exp_mul_fast<M>(xi, yi, p2, sm);
+      exp_sub_fast<M>(p1, p2, pre, sm);
+      exp_mul_fast<M>(xr, yi, p1, sm);
+      exp_mul_fast<M>(xi, yr, p2, sm);
+      exp_add_fast<M>(p1, p2, pim, sm);
+      if (i == 0) {
+        copy_md<M>(ar, pre);
+        copy_md<M>(ai, pim);
+      } else {
+        if (i == ia) {
+#pragma unroll
+          for (int q = 0; q < M; ++q) {
+            ar[q] = __ldcg(Z + q * S + k);
+            ai[q] = __ldcg(Z + (M + q) * S + k);
+          }
+        }
+        exp_add_fast<M>(ar, pre, ar, sm);
+        exp_add_fast<M>(ai, pim, ai, sm);
+      }
+      if (i == (second ? ibB : ibA)) {
+        store_md<M>(Z, S, k, ar);
+        store_md<M>(Z + M * S, S, k, ai);
+      }
+    }
+  }
+}
+
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kConvThreads, 4) k_conv_band(const BandArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm = make_lane(smem);
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= static_cast<int64_t>(a.batch) * a.ntasks) return;
+  const int tw = static_cast<int>(gw % a.ntasks);
+  band_task<M, CPLX, false>(a.arena, a.G, a.jobs, a.tasks[tw], gw / a.ntasks, threadIdx.x & 31, sm);
+}
+
+// Dataflow form of the banded convolution: ONE persistent launch. Warps take
+// work units (descriptor p of the scheduled order, point b) from a global
+// counter in order, wait until the units p depends on are done for point b
+// (acquire loads of their flags), run the task and publish their own flag
+// (stores, fence, release). A unit only waits for units earlier in the
+// order, which were taken by running warps before it, so the scheme cannot
+// deadlock; a wait that exceeds ~20 s traps instead of hanging the GPU.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kConvThreads, 4) k_conv_flow(const FlowArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm = make_lane(smem);
+  const int lane = threadIdx.x & 31;
+  const int64_t units = static_cast<int64_t>(a.nunits) * a.batch;
+  for (;;) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(a.counter, 1ull);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (static_cast<int64_t>(u) >= units) return;
+    const int p = static_cast<int>(u / a.batch);
+    const int64_t pt = static_cast<int64_t>(u % a.batch);
+    unsigned* fl = a.flags + pt * a.nunits;
+    for (int e = a.dep_off[p] + lane; e < a.dep_off[p + 1]; e += 32) {
+      const unsigned* f = fl + a.deps[e];
+      long long spins = 0;
+      while (ld_acquire(f) == 0u) {
+        __nanosleep(256);
+        if (++spins > (1ll << 26)) __trap();
+      }
+    }
+    __syncwarp();
+    band_task<M, CPLX, true>(a.arena, a.G, a.jobs, a.tasks[p], pt, lane, sm);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(fl + p, 1u);
   }
 }
 
@@ -508,6 +740,21 @@ struct Impl {
       default: k_conv<M, CPLX, 4><<<grid, kConvThreads, sh, s>>>(a); break;
     }
   }
+  static void conv_band(const BandArgs& a, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(a.batch) * a.ntasks * 32;
+    if (n == 0) return;
+    const size_t sh = smem_conv(kConvThreads);
+    k_conv_band<M, CPLX><<<static_cast<unsigned>((n + kConvThreads - 1) / kConvThreads), kConvThreads, sh, s>>>(a);
+  }
+  static void conv_flow(const FlowArgs& a, int blocks, cudaStream_t s) {
+    if (a.nunits == 0) return;
+    k_conv_flow<M, CPLX><<<blocks, kConvThreads, smem_conv(kConvThreads), s>>>(a);
+  }
+  static int band_blocks_per_sm() {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_conv_band<M, CPLX>, kConvThreads, smem_conv(kConvThreads));
+    return nb > 0 ? nb : 1;
+  }
   static void conv_prod(const SplitArgs& a, cudaStream_t s) {
     const int64_t n = static_cast<int64_t>(a.batch) * a.njobs * a.T;
     if (n == 0) return;
@@ -550,6 +797,8 @@ struct Impl {
     cudaFuncSetAttribute(k_conv<M, CPLX, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv<M, CPLX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv<M, CPLX, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
+    cudaFuncSetAttribute(k_conv_band<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
+    cudaFuncSetAttribute(k_conv_flow<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv_prod<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_conv_accum<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_add<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
@@ -558,7 +807,7 @@ struct Impl {
     cudaFuncSetAttribute(k_md<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
   }
   static const Launchers* table() {
-    static const Launchers L{&conv, &conv_prod, &conv_accum, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE};
+    static const Launchers L{&conv, &conv_band, &conv_flow, &band_blocks_per_sm, &conv_prod, &conv_accum, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE};
     return &L;
   }
 };

@@ -18,13 +18,21 @@ pytestmark = pytest.mark.gpu
 LEVELS = [1, 2, 3, 4, 5, 8, 10]
 
 
-@pytest.fixture(params=["fused", "split"])
+@pytest.fixture(params=["fused", "split", "band", "flow"])
 def conv_path(request, monkeypatch):
     """Run an engine test through the fused conv kernel (one thread per
-    coefficient pair) and through the split path (products in parallel, then
-    the accumulation chains). The planner reads PSE_SPLIT_THRESHOLD when a
-    plan is created: 0 forces fused, a huge value forces split."""
-    monkeypatch.setenv("PSE_SPLIT_THRESHOLD", "0" if request.param == "fused" else str(1 << 60))
+    coefficient pair), through the split path (products in parallel, then
+    the accumulation chains), through the banded wavefront (chains cut into
+    band x segment tasks, scheduled across layers, one launch per wave) and
+    through its dataflow form (one persistent launch, per-task completion
+    flags). The planner reads
+    PSE_CONV_MODE and PSE_SPLIT_THRESHOLD when a plan is created: 0 forces
+    fused, a huge value forces split."""
+    if request.param in ("band", "flow"):
+        monkeypatch.setenv("PSE_CONV_MODE", request.param)
+    else:
+        monkeypatch.setenv("PSE_CONV_MODE", "layer")
+        monkeypatch.setenv("PSE_SPLIT_THRESHOLD", "0" if request.param == "fused" else str(1 << 60))
     return request.param
 
 
@@ -167,6 +175,27 @@ def test_md_instances_bitwise_vs_oracle(m, cplx, conv_path):
         ref = po.evaluate(p, "port")
         vg, _ = dev_eval(p)
         assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"md instance m={m} cplx={cplx} it={it}")
+
+
+@pytest.mark.parametrize("pid,d,m", [("p2", 40, 2), ("p2", 70, 1), ("p1", 66, 2)])
+def test_multiband_graphs_bitwise(pid, d, m, conv_path):
+    """Degrees past one band (32 coefficients): the banded path cuts every
+    chain into segments and carries partial sums between waves."""
+    p = po.gen_benchmark(pid, d, m, seed=7)
+    ref = po.evaluate(p, "port")
+    vg, _ = dev_eval(p)
+    assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"{pid} d={d} m={m}")
+
+
+@pytest.mark.parametrize("m", LEVELS)
+@pytest.mark.parametrize("cplx", [False, True])
+def test_multiband_md_instances(m, cplx, conv_path):
+    rng = np.random.default_rng(1900 + m + 50 * cplx)
+    for it in range(4):
+        p = md_instance(rng, m, cplx, nmax=5, Nmax=5, dmin=33, dmax=100, with_exponents=it % 2 == 1)
+        ref = po.evaluate(p, "port")
+        vg, _ = dev_eval(p)
+        assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"md instance m={m} cplx={cplx} d={p.d} it={it}")
 
 
 def test_batched_points_equal_single_points(conv_path):
