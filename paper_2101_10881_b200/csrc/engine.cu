@@ -442,7 +442,7 @@ struct Plan {
   // host schedule + upload for a batch size (never during stream capture)
   void prepare_band(int batch) {
     if (!banded(batch) || band_waves.count(batch)) return;
-    const int warps = sms * L->band_blocks_per_sm() * (kLaneThreads / 32);
+    const int warps = sms * L->band_blocks_per_sm(flow()) * (kLaneThreads / 32);
     const int64_t cap2 = std::max<int64_t>(2, static_cast<int64_t>(2 * band_rounds * warps / batch));
     const BandSched sch = band_schedule(band_rows, d, cap2, flow(), std::max(1, warps / batch), flow_slack);
     std::vector<int4> all;
@@ -533,7 +533,7 @@ struct Plan {
         ck(cudaMemsetAsync(flow_flags, 0, sizeof(unsigned) * batch * bw.nunits, stream), "flags");
         ck(cudaMemsetAsync(flow_counter, 0, sizeof(unsigned long long), stream), "counter");
         FlowArgs a{arena, G, band_jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, flow_flags, flow_counter};
-        L->conv_flow(a, sms * L->band_blocks_per_sm(), stream);
+        L->conv_flow(a, sms * L->band_blocks_per_sm(true), stream);
         ++launches;
       } else {
         for (auto& [o, nw] : bw.waves) {

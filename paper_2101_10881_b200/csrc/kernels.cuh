@@ -135,7 +135,7 @@ struct Launchers {
   void (*conv)(const ConvArgs&, cudaStream_t);
   void (*conv_band)(const BandArgs&, cudaStream_t);
   void (*conv_flow)(const FlowArgs&, int blocks, cudaStream_t);
-  int (*band_blocks_per_sm)();
+  int (*band_blocks_per_sm)(bool flow);
   void (*conv_prod)(const SplitArgs&, cudaStream_t);
   void (*conv_accum)(const SplitArgs&, cudaStream_t);
   void (*add)(const AddArgs&, cudaStream_t);
@@ -300,17 +300,65 @@ __global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
 // COH (dataflow kernel): inputs produced by conv jobs (flag bits 1 and 2 of
 // the job's .w) may have been written during this kernel by other SMs and
 // are read through L2; static inputs keep the read-only path.
+// Dataflow tasks of short steps (M <= 4) stage their operand windows in
+// shared memory first -- the in1 segment (<= kBandW words per limb) and the
+// in2 range the task reads (<= 2*kBandW) -- so a task pays one L2 round trip
+// instead of one per step. kStageSlots words per limb and warp: rectangular
+// tasks use x [0,32) and y [32,96); diagonal half-warp h uses x [64h, 64h+32)
+// and y [64h+32, 64h+64).
+constexpr int kStageSlots = 128;
+template <int M, bool COH>
+__host__ __device__ constexpr bool band_stage() {
+  return COH && M <= 4;
+}
+
 template <int M, bool CPLX, bool COH>
 __device__ __forceinline__ void band_task(double* arena, const Geom& G, const int4* __restrict__ jobs, const int4 T,
-                                          int64_t pt, int lane, Lane sm) {
+                                          int64_t pt, int lane, Lane sm, double* __restrict__ stg) {
   const int S = G.S, d = G.d;
   constexpr int Q = CPLX ? 2 * M : M;
+  constexpr bool STAGE = band_stage<M, COH>();
   double* base = arena + pt * G.point_words;
   // band 0 is [0, W0) with W0 = d % kBandW + 1, the others are full
   const int W0 = d % kBandW + 1;
   const int width = T.y == 0 ? W0 : kBandW;
+  const bool diag = T.w != -1 && T.w != -3;
+  // staged windows: x_i at slot xo + i - xb, y_j at slot yo + j - yb
+  int xb = 0, yb = 0, xo = 0, yo = 0;
+  if constexpr (STAGE) {
+    if (T.w != -3) {
+      const int ws = T.z == 0 ? W0 : kBandW;  // segment width (rectangular)
+#pragma unroll 1
+      for (int h = 0; h < (diag ? 2 : 1); ++h) {
+        const int jh = h ? T.w : T.x;
+        if (jh < 0) continue;
+        const int4 Jh = jobs[jh];
+        const double* Xh = base + static_cast<int64_t>(Jh.x) * G.slot_words;
+        const double* Yh = base + static_cast<int64_t>(Jh.y) * G.slot_words;
+        const bool chx = COH && (Jh.w & 2), chy = COH && (Jh.w & 4);
+        const int hxb = diag ? T.y : T.z, hyb = diag ? 0 : T.y - T.z - ws + 1;
+        const int hxo = diag ? 64 * h : 0, hyo = hxo + 32, ny = diag ? 1 : 2;
+#pragma unroll 1
+        for (int q = 0; q < Q; ++q) {
+          const int ix = hxb + lane;
+          if (ix <= d) stg[q * kStageSlots + hxo + lane] = chx ? __ldcg(Xh + q * S + ix) : __ldg(Xh + q * S + ix);
+          for (int r = 0; r < ny; ++r) {
+            const int iy = hyb + 32 * r + lane;
+            if (iy >= 0 && iy <= d)
+              stg[q * kStageSlots + hyo + 32 * r + lane] = chy ? __ldcg(Yh + q * S + iy) : __ldg(Yh + q * S + iy);
+          }
+        }
+      }
+      const int h = diag ? lane >> 4 : 0;
+      xb = diag ? T.y : T.z;
+      yb = diag ? 0 : T.y - T.z - ws + 1;
+      xo = diag ? 64 * h : 0;
+      yo = xo + 32;
+    }
+    __syncwarp();
+  }
   int job = T.x, kA, iaA, ibA, kB = -1, iaB = 0, ibB = -1;
-  if (T.w == -1 || T.w == -3) {
+  if (!diag) {
     if (lane >= width) return;
     kA = T.y + lane;
     iaA = T.z;
@@ -338,6 +386,23 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
     for (int q = 0; q < Q; ++q) Z[q * S + kA] = cx ? __ldcg(X + q * S + kA) : X[q * S + kA];
     return;
   }
+  // operand loads: limb part*M+q of x_i / y_j
+  auto ldx = [&](int part, int i, double(&v)[M]) {
+    if constexpr (STAGE) {
+#pragma unroll
+      for (int q = 0; q < M; ++q) v[q] = stg[(part * M + q) * kStageSlots + xo + i - xb];
+    } else {
+      load_md_sel<M>(X + part * M * S, S, i, v, cx);
+    }
+  };
+  auto ldy = [&](int part, int j, double(&v)[M]) {
+    if constexpr (STAGE) {
+#pragma unroll
+      for (int q = 0; q < M; ++q) v[q] = stg[(part * M + q) * kStageSlots + yo + j - yb];
+    } else {
+      load_md_sel<M>(Y + part * M * S, S, j, v, cy);
+    }
+  };
   const int nA = ibA - iaA + 1;
   const int total = nA + (kB >= 0 ? ibB - iaB + 1 : 0);
   if constexpr (!CPLX) {
@@ -350,8 +415,8 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
       const int ia = second ? iaB : iaA;
       const int i = second ? iaB + (t - nA) : iaA + t;
       double xr[M], yr[M], p[M];
-      load_md_sel<M>(X, S, i, xr, cx);
-      load_md_sel<M>(Y, S, k - i, yr, cy);
+      ldx(0, i, xr);
+      ldy(0, k - i, yr);
       exp_mul_fast<M>(xr, yr, p, sm);
       if (i == 0) {
         copy_md<M>(o, p);
@@ -375,10 +440,10 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
       const int ia = second ? iaB : iaA;
       const int i = second ? iaB + (t - nA) : iaA + t;
       double xr[M], yr[M], xi[M], yi[M], p1[M], p2[M], pre[M], pim[M];
-      load_md_sel<M>(X, S, i, xr, cx);
-      load_md_sel<M>(Y, S, k - i, yr, cy);
-      load_md_sel<M>(X + M * S, S, i, xi, cx);
-      load_md_sel<M>(Y + M * S, S, k - i, yi, cy);
+      ldx(0, i, xr);
+      ldy(0, k - i, yr);
+      ldx(1, i, xi);
+      ldy(1, k - i, yi);
       exp_mul_fast<M>(xr, yr, p1, sm);
       exp_mul_fast<M>(xi, yi, p2, sm);
       exp_sub_fast<M>(p1, p2, pre, sm);
@@ -414,7 +479,7 @@ __global__ void __launch_bounds__(kConvThreads, 4) k_conv_band(const BandArgs a)
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (gw >= static_cast<int64_t>(a.batch) * a.ntasks) return;
   const int tw = static_cast<int>(gw % a.ntasks);
-  band_task<M, CPLX, false>(a.arena, a.G, a.jobs, a.tasks[tw], gw / a.ntasks, threadIdx.x & 31, sm);
+  band_task<M, CPLX, false>(a.arena, a.G, a.jobs, a.tasks[tw], gw / a.ntasks, threadIdx.x & 31, sm, nullptr);
 }
 
 // Dataflow form of the banded convolution: ONE persistent launch. Warps take
@@ -439,6 +504,10 @@ __global__ void __launch_bounds__(kConvThreads, 4) k_conv_flow(const FlowArgs a)
   const Lane sm = make_lane(smem);
   const int lane = threadIdx.x & 31;
   const int64_t units = static_cast<int64_t>(a.nunits) * a.batch;
+  // per-warp staging area after the lanes (band_stage)
+  constexpr int Q = CPLX ? 2 * M : M;
+  double* stg = smem + kLaneThreads * (CPLX ? MdTraits<M>::LANE : MdTraits<M>::LANE_CONV) +
+                (threadIdx.x >> 5) * kStageSlots * Q;
   for (;;) {
     unsigned long long u = 0;
     if (lane == 0) u = atomicAdd(a.counter, 1ull);
@@ -451,12 +520,13 @@ __global__ void __launch_bounds__(kConvThreads, 4) k_conv_flow(const FlowArgs a)
       const unsigned* f = fl + a.deps[e];
       long long spins = 0;
       while (ld_acquire(f) == 0u) {
-        __nanosleep(256);
-        if (++spins > (1ll << 26)) __trap();
+        __nanosleep(32);
+        if (++spins > (1ll << 28)) __trap();
       }
     }
     __syncwarp();
-    band_task<M, CPLX, true>(a.arena, a.G, a.jobs, a.tasks[p], pt, lane, sm);
+    band_task<M, CPLX, true>(a.arena, a.G, a.jobs, a.tasks[p], pt, lane, sm, stg);
+    __syncwarp();  // the staging area is rewritten by the next unit
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release(fl + p, 1u);
@@ -746,13 +816,23 @@ struct Impl {
     const size_t sh = smem_conv(kConvThreads);
     k_conv_band<M, CPLX><<<static_cast<unsigned>((n + kConvThreads - 1) / kConvThreads), kConvThreads, sh, s>>>(a);
   }
+  static size_t smem_flow() {
+    return smem_conv(kConvThreads) +
+           (band_stage<M, true>() ? static_cast<size_t>(kConvThreads / 32) * kStageSlots * (CPLX ? 2 * M : M) *
+                                        sizeof(double)
+                                  : 0);
+  }
   static void conv_flow(const FlowArgs& a, int blocks, cudaStream_t s) {
     if (a.nunits == 0) return;
-    k_conv_flow<M, CPLX><<<blocks, kConvThreads, smem_conv(kConvThreads), s>>>(a);
+    k_conv_flow<M, CPLX><<<blocks, kConvThreads, smem_flow(), s>>>(a);
   }
-  static int band_blocks_per_sm() {
+  // resident blocks per SM: banded waves (flow = false) or the dataflow kernel
+  static int band_blocks_per_sm(bool flow) {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_conv_band<M, CPLX>, kConvThreads, smem_conv(kConvThreads));
+    if (flow)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_conv_flow<M, CPLX>, kConvThreads, smem_flow());
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_conv_band<M, CPLX>, kConvThreads, smem_conv(kConvThreads));
     return nb > 0 ? nb : 1;
   }
   static void conv_prod(const SplitArgs& a, cudaStream_t s) {
@@ -798,7 +878,8 @@ struct Impl {
     cudaFuncSetAttribute(k_conv<M, CPLX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv<M, CPLX, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv_band<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
-    cudaFuncSetAttribute(k_conv_flow<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
+    cudaFuncSetAttribute(k_conv_flow<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem_flow()));
     cudaFuncSetAttribute(k_conv_prod<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_conv_accum<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
     cudaFuncSetAttribute(k_add<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
