@@ -194,12 +194,20 @@ def conv_alg_ops(g, d: int, m: int) -> int:
     return C * ((d + 1) * (d + 2) // 2 * c.mul_cost + d * (d + 1) // 2 * c.add_cost)
 
 
-def load_traffic():
-    path = os.path.join(ROOT, "profiles", "ncu_conv_summary.json")
+def load_traffic(wl: str, path: str):
+    """DRAM bytes of the conv stage per evaluation point for this workload and
+    conv path, from the committed ncu captures (profiles/ncu_traffic.json)."""
     try:
-        return json.load(open(path)).get("dram_bytes_per_launch")
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[f"{wl}/{path}"]["dram_bytes_per_eval"]
     except Exception:
         return None
+
+
+CONV_KERNEL = {
+    "layered": "k_conv<{m},real> (one launch per conv layer and monomial group; split prod/accum for small layers)",
+    "waves": "k_conv_band<{m},real> (one launch per scheduled wave of band x segment tasks)",
+    "dataflow": "k_conv_flow<{m},real> (one persistent launch per evaluation wave)",
+}
 
 
 def ours(args, wl):
@@ -292,7 +300,7 @@ def ours(args, wl):
     ms_per_step = total_ms / args.steps
     value = model_ops * total_points * args.steps / (total_ms * 1e-3) / 1e12
     conv_ms = sum(convs)
-    n_conv_launch = len(g.conv_layer_sizes()) * len(waves) * args.steps
+    path = plan.conv_path(wave)
     achieved = conv_ops * len(mine) * args.steps / (conv_ms * 1e-3)
 
     # ---- e2e: public C-ABI call with pinned host buffers, one wave per call
@@ -336,12 +344,13 @@ def ours(args, wl):
         "alg_ops_per_eval": alg_ops,
         "conv_alg_ops_per_eval": conv_ops,
         "roofline": {
-            "bound": "fp64", "kernel": f"k_conv<{m},real> (all conv layers)",
+            "bound": "fp64", "kernel": CONV_KERNEL[path].format(m=m), "conv_path": path,
             "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s (binary64, algorithmic)",
-            "frac": achieved / peak_ops, "traffic": load_traffic(),
+            "frac": achieved / peak_ops, "traffic": load_traffic(wl, path),
+            "traffic_unit": "DRAM bytes of the conv stage per evaluation point (ncu, profiles/ncu_traffic.json)",
             "peak_source": "measured live: pse_fp64_peak (independent DADD/DFMA chains on every SM)",
-            "per_launch_ms": conv_ms / max(1, n_conv_launch),
-            "alg_ops_per_launch": conv_ops * len(mine) / max(1, len(g.conv_layer_sizes())),
+            "conv_ms_per_eval": conv_ms / (len(mine) * args.steps),
+            "alg_ops_per_eval": conv_ops,
         },
         "e2e": {"value": e2e_value, "unit": "TFLOPS", "ms_per_call": e2e_total / args.steps,
                 "h2d_bytes_per_step": int(Q * nb * pw * 8), "d2h_bytes_per_step": int(Q * nb * (n + 1) * (d + 1) * 8)},

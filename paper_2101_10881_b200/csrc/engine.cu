@@ -1250,6 +1250,13 @@ int pse_plan_stream(const pse_plan* p, void** stream) {
   return PSE_OK;
 }
 
+int pse_plan_conv_path(const pse_plan* p, int32_t batch, int32_t* path) {
+  if (!p || !path || batch < 1 || batch > p->p->max_batch) return PSE_EINVAL;
+  const pse::Plan& P = *p->p;
+  *path = !P.banded(batch) ? PSE_CONV_LAYERED : P.flow() ? PSE_CONV_DATAFLOW : PSE_CONV_WAVES;
+  return PSE_OK;
+}
+
 int pse_plan_info(const pse_plan* p, int64_t* out) {
   if (!p || !out) return PSE_EINVAL;
   const pse::Plan& P = *p->p;
