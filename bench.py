@@ -207,6 +207,7 @@ CONV_KERNEL = {
     "layered": "k_conv<{m},real> (one launch per conv layer and monomial group; split prod/accum for small layers)",
     "waves": "k_conv_band<{m},real> (one launch per scheduled wave of band x segment tasks)",
     "dataflow": "k_conv_flow<{m},real> (one persistent launch per evaluation wave)",
+    "hybrid": "k_conv<{m},real> for the large conv layers, then k_conv_flow<{m},real> for the trailing small ones",
 }
 
 

@@ -192,9 +192,11 @@ int pse_plan_stream(const pse_plan* p, void** stream);
 /* which convolution path a run of `batch` points takes (no reference
  * counterpart; for reporting): PSE_CONV_LAYERED (one launch per dependency
  * level, concurrent monomial groups, split chains for small layers),
- * PSE_CONV_WAVES (band x segment tasks, one launch per scheduled wave) or
- * PSE_CONV_DATAFLOW (the same tasks in one persistent launch) */
-enum { PSE_CONV_LAYERED = 1, PSE_CONV_WAVES = 2, PSE_CONV_DATAFLOW = 3 };
+ * PSE_CONV_WAVES (band x segment tasks, one launch per scheduled wave),
+ * PSE_CONV_DATAFLOW (the same tasks in one persistent launch) or
+ * PSE_CONV_HYBRID (layered for the large layers, then one dataflow launch
+ * for the trailing small ones) */
+enum { PSE_CONV_LAYERED = 1, PSE_CONV_WAVES = 2, PSE_CONV_DATAFLOW = 3, PSE_CONV_HYBRID = 4 };
 int pse_plan_conv_path(const pse_plan* p, int32_t batch, int32_t* path);
 
 /* evaluate() (executor.cpp:271-276): build graph, fold exponents (on the

@@ -376,6 +376,7 @@ struct Plan {
   // monomials) whose layer sequences run concurrently on their own streams.
   struct ConvGroup {
     std::vector<std::pair<int4*, int>> layers;  // (jobs, njobs) per layer
+    std::vector<int> layer_index;                // graph conv layer of each entry
     cudaStream_t stream = nullptr;
     cudaEvent_t join = nullptr;
     double* prod = nullptr;  // split-path scratch of this group
@@ -408,12 +409,14 @@ struct Plan {
   int64_t flops_model = 0, alg_ops = 0, conv_jobs = 0, add_jobs = 0, copy_jobs = 0;
   std::map<int, cudaGraphExec_t> graphs;
   std::vector<cudaEvent_t> ev;
-  // Banded conv stage (deep graphs with few jobs per layer, see BandArgs):
-  // this rank's non-prologue conv jobs in layer order, their device table,
-  // and per batch size the task waves (one launch each).
-  std::vector<ConvRow> band_rows;
-  int4* band_jobs = nullptr;
+  // Banded conv stage (see BandArgs): this rank's non-prologue conv jobs per
+  // graph layer, and per batch size the banded part -- the conv layers from
+  // `first` on, their job table and task schedule.
+  std::vector<std::vector<ConvRow>> layer_rows;
+  int64_t nrows_mine = 0;
   struct BandWaves {
+    int first = 0;
+    int4* jobs = nullptr;
     int4* tasks = nullptr;
     std::vector<std::pair<int64_t, int>> waves;  // (offset, warps)
     int* dep_off = nullptr;  // flow mode
@@ -429,24 +432,45 @@ struct Plan {
   double flow_slack = 0.3;   // PSE_FLOW_SLACK: see band_schedule
   int64_t layer_pairs = 0;   // average conv layer size in coefficient pairs
 
-  // Layered when the average conv layer offers at least two waves of
-  // resident threads (one per coefficient pair), banded otherwise.
-  bool banded(int batch) const {
-    if (band_rows.empty() || conv_mode == 1) return false;
-    if (conv_mode >= 2) return true;
-    return static_cast<int64_t>(batch) * layer_pairs < int64_t(sms) * 4 * 128 * 2;
+  // First conv layer the banded path runs for this batch (layer_rows.size():
+  // none). A layer is "small" when it offers less than two waves of resident
+  // threads at one thread per coefficient pair. Deep graphs whose average
+  // layer is small run banded throughout; otherwise the trailing run of small
+  // layers (e.g. C2's last layer) runs banded after the layered ones.
+  int band_first(int batch) const {
+    const int nl = static_cast<int>(layer_rows.size());
+    if (nrows_mine == 0 || conv_mode == 1) return nl;
+    if (conv_mode >= 2) return 0;
+    const int64_t thr = int64_t(sms) * 4 * 128 * 2, npairs = (d + 2) / 2;
+    if (static_cast<int64_t>(batch) * layer_pairs < thr) return 0;
+    int f = nl;
+    while (f > 0 && static_cast<int64_t>(batch) * static_cast<int64_t>(layer_rows[f - 1].size()) * npairs < thr) --f;
+    return f;
   }
+  bool banded(int batch) const { return band_first(batch) < static_cast<int>(layer_rows.size()); }
 
   bool flow() const { return conv_mode == 3 || conv_mode == 0; }
 
   // host schedule + upload for a batch size (never during stream capture)
   void prepare_band(int batch) {
     if (!banded(batch) || band_waves.count(batch)) return;
+    BandWaves bw;
+    bw.first = band_first(batch);
+    std::vector<ConvRow> rows;
+    for (size_t L2 = bw.first; L2 < layer_rows.size(); ++L2) rows.insert(rows.end(), layer_rows[L2].begin(), layer_rows[L2].end());
+    {  // job table; flag bits 2/4: in1/in2 produced inside the banded part
+      std::set<int64_t> produced;
+      for (auto& r : rows) produced.insert(r.out);
+      std::vector<int4> v;
+      for (auto& r : rows)
+        v.push_back(make_int4(static_cast<int>(r.in1), static_cast<int>(r.in2), static_cast<int>(r.out),
+                              (produced.count(r.in1) ? 2 : 0) | (!r.copy && produced.count(r.in2) ? 4 : 0)));
+      bw.jobs = dev_upload(v, stream);
+    }
     const int warps = sms * L->band_blocks_per_sm(flow()) * (kLaneThreads / 32);
     const int64_t cap2 = std::max<int64_t>(2, static_cast<int64_t>(2 * band_rounds * warps / batch));
-    const BandSched sch = band_schedule(band_rows, d, cap2, flow(), std::max(1, warps / batch), flow_slack);
+    const BandSched sch = band_schedule(rows, d, cap2, flow(), std::max(1, warps / batch), flow_slack);
     std::vector<int4> all;
-    BandWaves bw;
     for (auto& w : sch.waves) {
       bw.waves.emplace_back(static_cast<int64_t>(all.size()), static_cast<int>(w.size()));
       all.insert(all.end(), w.begin(), w.end());
@@ -473,6 +497,7 @@ struct Plan {
     for (auto& [b, g] : graphs) cudaGraphExecDestroy(g);
     for (auto& [b, w] : band_waves) {
       cudaFree(w.tasks);
+      cudaFree(w.jobs);
       cudaFree(w.dep_off);
       cudaFree(w.deps);
     }
@@ -527,34 +552,41 @@ struct Plan {
   int launch_conv(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
     int launches = 0;
     for (auto& [jobs, nj] : pro_layers) launches += launch_layer(jobs, nj, batch, groups[0], stream);
-    if (banded(batch)) {
+    const int first = band_first(batch);
+    if (first > 0) {  // layered part: graph conv layers < first
+      if (groups.size() == 1) {
+        for (size_t q = 0; q < groups[0].layers.size(); ++q) {
+          if (groups[0].layer_index[q] >= first) continue;
+          launches += launch_layer(groups[0].layers[q].first, groups[0].layers[q].second, batch, groups[0], stream);
+          if (marks) mark(marks, 'c');
+        }
+      } else {
+        ck(cudaEventRecord(fork, stream), "fork");
+        for (ConvGroup& gr : groups) {
+          ck(cudaStreamWaitEvent(gr.stream, fork, 0), "fork wait");
+          for (size_t q = 0; q < gr.layers.size(); ++q)
+            if (gr.layer_index[q] < first)
+              launches += launch_layer(gr.layers[q].first, gr.layers[q].second, batch, gr, gr.stream);
+          ck(cudaEventRecord(gr.join, gr.stream), "join");
+          ck(cudaStreamWaitEvent(stream, gr.join, 0), "join wait");
+        }
+        if (marks) mark(marks, 'c');
+      }
+    }
+    if (first < static_cast<int>(layer_rows.size())) {  // banded part
       const BandWaves& bw = band_waves.at(batch);
       if (flow()) {
         ck(cudaMemsetAsync(flow_flags, 0, sizeof(unsigned) * batch * bw.nunits, stream), "flags");
         ck(cudaMemsetAsync(flow_counter, 0, sizeof(unsigned long long), stream), "counter");
-        FlowArgs a{arena, G, band_jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, flow_flags, flow_counter};
+        FlowArgs a{arena, G, bw.jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, flow_flags, flow_counter};
         L->conv_flow(a, sms * L->band_blocks_per_sm(true), stream);
         ++launches;
       } else {
         for (auto& [o, nw] : bw.waves) {
-          BandArgs a{arena, G, band_jobs, bw.tasks + o, nw, batch};
+          BandArgs a{arena, G, bw.jobs, bw.tasks + o, nw, batch};
           L->conv_band(a, stream);
           ++launches;
         }
-      }
-      if (marks) mark(marks, 'c');
-    } else if (groups.size() == 1) {
-      for (auto& [jobs, nj] : groups[0].layers) {
-        launches += launch_layer(jobs, nj, batch, groups[0], stream);
-        if (marks) mark(marks, 'c');
-      }
-    } else {
-      ck(cudaEventRecord(fork, stream), "fork");
-      for (ConvGroup& gr : groups) {
-        ck(cudaStreamWaitEvent(gr.stream, fork, 0), "fork wait");
-        for (auto& [jobs, nj] : gr.layers) launches += launch_layer(jobs, nj, batch, gr, gr.stream);
-        ck(cudaEventRecord(gr.join, gr.stream), "join");
-        ck(cudaStreamWaitEvent(stream, gr.join, 0), "join wait");
       }
       if (marks) mark(marks, 'c');
     }
@@ -601,9 +633,12 @@ struct Plan {
   int kernel_count(int batch) const {
     int n = nranks > 1 ? 0 : (nts ? 1 : 0) + static_cast<int>(add_layers.size()) + 1;
     for (auto& [jobs, nj] : pro_layers) n += split_layer(nj, batch, groups[0]) ? 2 : 1;
-    if (banded(batch)) return n + (flow() ? 1 : static_cast<int>(band_waves.at(batch).waves.size()));
+    const int first = band_first(batch);
+    if (first < static_cast<int>(layer_rows.size()))
+      n += flow() ? 1 : static_cast<int>(band_waves.at(batch).waves.size());
     for (const ConvGroup& gr : groups)
-      for (auto& [jobs, nj] : gr.layers) n += split_layer(nj, batch, gr) ? 2 : 1;
+      for (size_t q = 0; q < gr.layers.size(); ++q)
+        if (gr.layer_index[q] < first) n += split_layer(gr.layers[q].second, batch, gr) ? 2 : 1;
     return n;
   }
 };
@@ -764,26 +799,23 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
     int64_t nlayers = 0;
     for (size_t L = npro; L < layers.size(); ++L) {
       std::vector<std::vector<ConvRow>> per(ng);
+      p->layer_rows.emplace_back();
       for (const ConvRow& r : layers[L]) {
         auto it = comp_group.find(find(r.out));
         if (it != comp_group.end()) {
           per[it->second].push_back(r);
-          p->band_rows.push_back(r);
+          p->layer_rows.back().push_back(r);
+          ++p->nrows_mine;
         }
       }
       if (!layers[L].empty()) ++nlayers;
       for (int gi = 0; gi < ng; ++gi)
-        if (!per[gi].empty()) p->groups[gi].layers.push_back(upload_rows(per[gi]));
+        if (!per[gi].empty()) {
+          p->groups[gi].layers.push_back(upload_rows(per[gi]));
+          p->groups[gi].layer_index.push_back(static_cast<int>(L - npro));
+        }
     }
-    p->layer_pairs = static_cast<int64_t>(p->band_rows.size()) * ((g.d + 2) / 2) / std::max<int64_t>(1, nlayers);
-    if (!p->band_rows.empty()) {
-      std::vector<int4> v;
-      for (auto& r : p->band_rows)
-        v.push_back(make_int4(static_cast<int>(r.in1), static_cast<int>(r.in2), static_cast<int>(r.out),
-                              (r.in1 >= top ? 2 : 0) | (!r.copy && r.in2 >= top ? 4 : 0)));
-      p->band_jobs = dev_upload(v, s);
-      p->owned.push_back(p->band_jobs);
-    }
+    p->layer_pairs = p->nrows_mine * ((g.d + 2) / 2) / std::max<int64_t>(1, nlayers);
     {
       const char* cm = getenv("PSE_CONV_MODE");
       const std::string m = cm ? cm : "";
@@ -1253,7 +1285,10 @@ int pse_plan_stream(const pse_plan* p, void** stream) {
 int pse_plan_conv_path(const pse_plan* p, int32_t batch, int32_t* path) {
   if (!p || !path || batch < 1 || batch > p->p->max_batch) return PSE_EINVAL;
   const pse::Plan& P = *p->p;
-  *path = !P.banded(batch) ? PSE_CONV_LAYERED : P.flow() ? PSE_CONV_DATAFLOW : PSE_CONV_WAVES;
+  *path = !P.banded(batch)          ? PSE_CONV_LAYERED
+          : !P.flow()               ? PSE_CONV_WAVES
+          : P.band_first(batch) > 0 ? PSE_CONV_HYBRID
+                                    : PSE_CONV_DATAFLOW;
   return PSE_OK;
 }
 

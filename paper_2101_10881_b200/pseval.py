@@ -442,11 +442,11 @@ class DevicePlan:
         check(lib().pse_plan_stream(self._h, C.byref(s)))
         return s.value or 0
 
-    CONV_PATHS = {1: "layered", 2: "waves", 3: "dataflow"}
+    CONV_PATHS = {1: "layered", 2: "waves", 3: "dataflow", 4: "hybrid"}
 
     def conv_path(self, batch: int = 1) -> str:
         """the convolution path a run of `batch` points takes
-        (pse_plan_conv_path): layered, waves or dataflow"""
+        (pse_plan_conv_path): layered, waves, dataflow or hybrid"""
         v = C.c_int32()
         check(lib().pse_plan_conv_path(self._h, batch, C.byref(v)))
         return self.CONV_PATHS[v.value]
