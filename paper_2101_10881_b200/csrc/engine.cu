@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -140,27 +141,32 @@ T* dev_upload(const std::vector<T>& v, cudaStream_t s) {
   return p;
 }
 
-// Banded conv schedule (see BandArgs in kernels.cuh). Tasks (job, band b,
-// segment s <= b) -- one per band for copy jobs -- with the dependencies:
+// Banded conv schedule (see BandArgs in kernels.cuh), band width W. Tasks
+// (job, band b, segment s <= b) -- one per band for copy jobs -- with the
+// dependencies:
 //   (J, b, s-1)                   the running sum of the same chains;
 //   final band s of in1's job     steps i in segment s read x_i, i in band s;
 //   final bands <= b of in2's job (segment 0; later segments read less);
 // where "final band b" of a job is its task (b, b) (copy: its band-b task).
-// Static inputs and prologue outputs are ready before the first wave. Tasks
-// are list-scheduled into waves of at most `cap2` half-warps (a rectangular
-// or copy task fills a warp, a diagonal task half of one), highest
-// longest-path-to-exit first; each wave becomes one launch (banded mode), or
-// the waves, flattened, are the order in which the dataflow kernel hands out
-// descriptors (flow mode; the per-descriptor dependency lists serve it).
+// Static inputs and outputs of earlier launches are ready from the start.
+// Tasks are ranked by longest path to the exit. Wave mode: list-scheduled
+// into waves of at most `cap_slots` 8-lane slots, one launch per wave. Flow
+// mode: greedy list scheduling simulated in time gives the order in which
+// the dataflow kernel hands out warp descriptors. Tasks are packed into
+// descriptors of kSlots slots in that order (a task only joins the open
+// descriptor if none of its dependencies is in it).
 struct BandSched {
-  std::vector<std::vector<int4>> waves;  // warp descriptors per wave
-  std::vector<int> dep_off, deps;        // per descriptor (numbered in wave order): descriptors it waits for
+  std::vector<std::vector<int4>> waves;  // kSlots slots per warp descriptor, per wave
+  std::vector<int> dep_off, deps;        // per descriptor (numbered in order): descriptors it waits for
+  double makespan = 0;                   // flow: simulated, in steps (one step = one md_mul + md_add)
 };
 
-BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int64_t cap2, bool flow, int64_t procs, double slack) {
-  const int nb = 1 + d / kBandW;  // band 0 = [0, d % W + 1), then full bands (kernels.cuh)
-  const int W0 = d % kBandW + 1;
-  auto lo = [&](int b) { return b == 0 ? 0 : W0 + (b - 1) * kBandW; };
+// ovh: fixed cost of a task (hand-out, dependency flags, partial sums) in steps
+BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int W, int64_t cap_slots, bool flow, int64_t procs,
+                        double slack, double ovh) {
+  const int nb = 1 + d / W;  // band 0 = [0, d % W + 1), then full bands (kernels.cuh)
+  const int W0 = d % W + 1;
+  auto lo = [&](int b) { return b == 0 ? 0 : W0 + (b - 1) * W; };
   const int nj = static_cast<int>(rows.size());
   std::map<int64_t, int> producer;
   for (int j = 0; j < nj; ++j) producer[rows[j].out] = j;
@@ -197,45 +203,92 @@ BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int64_t cap2, b
       }
     }
   }
-  // successor lists (CSR); every edge goes from a lower to a higher task id
-  std::vector<int64_t> off(T + 1, 0), succ(edges.size());
+  // successor and predecessor lists (CSR); every edge goes from a lower to a
+  // higher task id, so ids are a topological order
+  std::vector<int64_t> off(T + 1, 0), succ(edges.size()), poff(T + 1, 0), pred(edges.size());
   std::vector<int> indeg(T, 0);
-  for (auto& e : edges) ++off[e.first + 1], ++indeg[e.second];
-  for (int64_t t = 0; t < T; ++t) off[t + 1] += off[t];
+  for (auto& e : edges) ++off[e.first + 1], ++poff[e.second + 1], ++indeg[e.second];
+  for (int64_t t = 0; t < T; ++t) off[t + 1] += off[t], poff[t + 1] += poff[t];
   {
-    std::vector<int64_t> fill(off.begin(), off.end() - 1);
-    for (auto& e : edges) succ[fill[e.first]++] = e.second;
+    std::vector<int64_t> f1(off.begin(), off.end() - 1), f2(poff.begin(), poff.end() - 1);
+    for (auto& e : edges) succ[f1[e.first]++] = e.second, pred[f2[e.second]++] = e.first;
   }
   std::vector<int> prio(T, 1);
   for (int64_t t = T - 1; t >= 0; --t)
     for (int64_t e = off[t]; e < off[t + 1]; ++e) prio[t] = std::max(prio[t], prio[succ[e]] + 1);
-  // predecessor lists (descriptor dependencies, pairing checks)
-  std::vector<int64_t> poff(T + 1, 0), pred(edges.size());
-  for (auto& e : edges) ++poff[e.second + 1];
-  for (int64_t t = 0; t < T; ++t) poff[t + 1] += poff[t];
-  {
-    std::vector<int64_t> fill(poff.begin(), poff.end() - 1);
-    for (auto& e : edges) pred[fill[e.second]++] = e.first;
-  }
   auto is_diag = [&](int64_t t) { return ts[t] >= 0 && ts[t] == tb[t]; };
-  BandSched out;
-  std::vector<int> desc_of(T, -1);
-  std::vector<std::pair<int64_t, int64_t>> members;  // tasks of each descriptor (second = -1: none)
-  auto desc_for = [&](int64_t t, int64_t t2) {
+  double makespan = 0;
+  {  // makespan estimate in steps: max(critical path, work / warps), tasks
+     // weighted by their steps plus the fixed cost ovh
+    std::vector<double> cp(T, 0.0);
+    double work = 0, crit = 0;
+    for (int64_t t = T - 1; t >= 0; --t) {
+      const int wb = tb[t] == 0 ? W0 : W, wsg = ts[t] == 0 ? W0 : W;
+      const double steps = (ts[t] < 0 ? 1.0 : is_diag(t) ? wb + 1.0 : double(wsg)) + ovh;
+      work += steps * (is_diag(t) ? W / 2 : W) / 32.0;
+      double best = 0;
+      for (int64_t e = off[t]; e < off[t + 1]; ++e) best = std::max(best, cp[succ[e]]);
+      cp[t] = steps + best;
+      crit = std::max(crit, cp[t]);
+    }
+    makespan = std::max(crit, work / std::max<double>(1.0, procs * W / 32.0));
+  }
+  auto span = [&](int64_t t) { return is_diag(t) ? W / 16 : W / 8; };  // slots
+  auto slot_of = [&](int64_t t) {
     const int j = tjob[t], b = tb[t], s2 = ts[t];
     if (s2 < 0) return make_int4(j, lo(b), 0, -3);
     if (s2 < b) return make_int4(j, lo(b), lo(s2), -1);
-    return make_int4(j, lo(b), lo(b), t2 >= 0 ? tjob[t2] : -2);
+    return make_int4(j, lo(b), lo(b), -2);
   };
-  auto add_desc = [&](std::vector<int4>& w, int64_t t1, int64_t t2) {
-    desc_of[t1] = static_cast<int>(members.size());
-    if (t2 >= 0) desc_of[t2] = static_cast<int>(members.size());
-    members.emplace_back(t1, t2);
-    w.push_back(desc_for(t1, t2));
+
+  // Packing into warp descriptors: a task goes to the earliest of the last
+  // kOpen descriptors that has an aligned free position and follows all its
+  // dependencies' descriptors, else to a new descriptor.
+  BandSched out;
+  out.makespan = makespan;
+  std::vector<int> desc_of(T, -1);
+  std::vector<std::array<int64_t, kSlots>> members;
+  constexpr int kOpen = 64;
+  std::vector<std::pair<int, unsigned>> openl;  // (descriptor, used-slot mask), ascending
+  auto place = [&](std::vector<int4>& w, size_t wfirst, int64_t t) {
+    const int sp = span(t);
+    int latest = -1;
+    for (int64_t e = poff[t]; e < poff[t + 1]; ++e) latest = std::max(latest, desc_of[pred[e]]);
+    const int lim = static_cast<int>(members.size()) - kOpen;
+    int dsc = -1, pos = -1;
+    size_t oi = 0;
+    for (; oi < openl.size(); ++oi) {
+      const auto [q, used] = openl[oi];
+      if (q <= latest || q < lim || q < static_cast<int>(wfirst)) continue;
+      for (int f = 0; f + sp <= kSlots; f += sp)
+        if (((used >> f) & ((1u << sp) - 1)) == 0) {
+          dsc = q, pos = f;
+          break;
+        }
+      if (dsc >= 0) break;
+    }
+    if (dsc < 0) {
+      dsc = static_cast<int>(members.size());
+      members.emplace_back();
+      members.back().fill(-1);
+      for (int f = 0; f < kSlots; ++f) w.push_back(make_int4(0, 0, 0, -4));
+      openl.emplace_back(dsc, 0u);
+      oi = openl.size() - 1;
+      pos = 0;
+    }
+    const int4 v = slot_of(t);
+    const size_t wb = (static_cast<size_t>(dsc) - wfirst) * kSlots;
+    for (int f = pos; f < pos + sp; ++f) w[wb + f] = v;
+    openl[oi].second |= ((1u << sp) - 1) << pos;
+    members[dsc][pos] = t;
+    desc_of[t] = dsc;
+    if (openl[oi].second == (1u << kSlots) - 1) openl.erase(openl.begin() + static_cast<long>(oi));
+    while (!openl.empty() && openl.front().first < static_cast<int>(members.size()) - kOpen) openl.erase(openl.begin());
   };
+
   if (flow) {
-    // Greedy list scheduling simulated in time on `procs` warps (a task
-    // lasts its steps / kBandW; a diagonal task, half a warp, half that);
+    // Greedy list scheduling simulated in time on `procs` task processors (a
+    // task lasts its steps / W; a diagonal task, half the lanes, half that);
     // a task becomes ready `slack` after its last dependency finishes, so
     // in the resulting hand-out order a unit's dependencies are, where the
     // graph allows, a little more than one round of warps earlier.
@@ -248,9 +301,9 @@ BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int64_t cap2, b
     for (int64_t q = 0; q < std::max<int64_t>(1, procs); ++q) procfree.push(0.0);
     for (int64_t t = 0; t < T; ++t)
       if (indeg2[t] == 0) pending.emplace(0.0, t);
-    std::vector<int64_t> order;
-    order.reserve(T);
-    while (static_cast<int64_t>(order.size()) < T) {
+    std::vector<int4> w;
+    int64_t placed = 0;
+    while (placed < T) {
       double now = procfree.top();
       while (!pending.empty() && pending.top().first <= now) {
         ready.emplace(prio[pending.top().second], -pending.top().second);
@@ -265,48 +318,20 @@ BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int64_t cap2, b
       const int64_t t = -ready.top().second;
       ready.pop();
       procfree.pop();
-      const int wb = tb[t] == 0 ? W0 : kBandW, wsg = ts[t] == 0 ? W0 : kBandW;
-      const double dur = ts[t] < 0 ? 0.1 : is_diag(t) ? (wb + 1) / (2.0 * kBandW) : double(wsg) / kBandW;
+      const int wb = tb[t] == 0 ? W0 : W, wsg = ts[t] == 0 ? W0 : W;
+      const double dur = ts[t] < 0 ? 0.1 : is_diag(t) ? (wb + 1) / (2.0 * W) : double(wsg) / W;
       const double fin = now + dur;
       procfree.push(fin);
-      order.push_back(t);
+      place(w, 0, t);
+      ++placed;
       for (int64_t e = off[t]; e < off[t + 1]; ++e) {
         const int64_t u = succ[e];
         rt[u] = std::max(rt[u], fin + slack);
         if (--indeg2[u] == 0) pending.emplace(rt[u], u);
       }
     }
-    // descriptors in that order; a diagonal task joins the last open
-    // diagonal descriptor of its band (at most 64 descriptors back) when
-    // all its dependencies precede that descriptor
-    std::vector<int4> w;
-    std::map<int, int> open;  // band -> descriptor with a free half
-    for (int64_t t : order) {
-      if (!is_diag(t)) {
-        add_desc(w, t, -1);
-        continue;
-      }
-      const auto it = open.find(tb[t]);
-      bool joined = false;
-      if (it != open.end() && static_cast<int>(members.size()) - it->second <= 64) {
-        int latest = -1;
-        for (int64_t e = poff[t]; e < poff[t + 1]; ++e) latest = std::max(latest, desc_of[pred[e]]);
-        if (latest < it->second) {
-          members[it->second].second = t;
-          desc_of[t] = it->second;
-          w[it->second].w = tjob[t];
-          open.erase(it);
-          joined = true;
-        }
-      }
-      if (!joined) {
-        open[tb[t]] = static_cast<int>(members.size());
-        add_desc(w, t, -1);
-      }
-    }
     out.waves.push_back(std::move(w));
   } else {
-    auto cost = [&](int64_t t) { return is_diag(t) ? 1 : 2; };
     std::vector<int> indeg2 = indeg;
     std::priority_queue<std::pair<int, int64_t>> ready;  // (prio, -id)
     for (int64_t t = 0; t < T; ++t)
@@ -315,23 +340,18 @@ BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int64_t cap2, b
     while (done < T) {
       if (ready.empty()) throw std::logic_error("band schedule: dependency cycle");
       std::vector<int64_t> picked;
-      int64_t used = 0;
-      while (!ready.empty() && used + cost(-ready.top().second) <= std::max<int64_t>(cap2, 2)) {
+      int64_t usedc = 0;
+      while (!ready.empty() && usedc + span(-ready.top().second) <= std::max<int64_t>(cap_slots, kSlots)) {
         const int64_t t = -ready.top().second;
         ready.pop();
-        used += cost(t);
+        usedc += span(t);
         picked.push_back(t);
       }
+      // tasks of one wave are independent; pack the wide ones first
+      std::stable_sort(picked.begin(), picked.end(), [&](int64_t x, int64_t y) { return span(x) > span(y); });
       std::vector<int4> w;
-      std::map<int, std::vector<int64_t>> diag;  // band -> tasks
-      for (int64_t t : picked) {
-        if (is_diag(t))
-          diag[tb[t]].push_back(t);
-        else
-          add_desc(w, t, -1);
-      }
-      for (auto& [b, ts2] : diag)
-        for (size_t q = 0; q < ts2.size(); q += 2) add_desc(w, ts2[q], q + 1 < ts2.size() ? ts2[q + 1] : -1);
+      const size_t wfirst = members.size();  // descriptors of earlier waves are closed
+      for (int64_t t : picked) place(w, wfirst, t);
       out.waves.push_back(std::move(w));
       for (int64_t t : picked)
         for (int64_t e = off[t]; e < off[t + 1]; ++e)
@@ -343,7 +363,7 @@ BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int64_t cap2, b
   out.dep_off.assign(1, 0);
   for (size_t dsc = 0; dsc < members.size(); ++dsc) {
     std::vector<int> ds;
-    for (int64_t t : {members[dsc].first, members[dsc].second}) {
+    for (int64_t t : members[dsc]) {
       if (t < 0) continue;
       for (int64_t e = poff[t]; e < poff[t + 1]; ++e) {
         const int q = desc_of[pred[e]];
@@ -416,9 +436,10 @@ struct Plan {
   int64_t nrows_mine = 0;
   struct BandWaves {
     int first = 0;
+    int W = 32;
     int4* jobs = nullptr;
     int4* tasks = nullptr;
-    std::vector<std::pair<int64_t, int>> waves;  // (offset, warps)
+    std::vector<std::pair<int64_t, int>> waves;  // (first descriptor, descriptors)
     int* dep_off = nullptr;  // flow mode
     int* deps = nullptr;
     int nunits = 0;
@@ -430,6 +451,7 @@ struct Plan {
   int conv_mode = 0;         // PSE_CONV_MODE: 0 auto, 1 layered, 2 banded waves, 3 dataflow
   double band_rounds = 1.0;  // PSE_BAND_ROUNDS: wave size in resident warps
   double flow_slack = 0.3;   // PSE_FLOW_SLACK: see band_schedule
+  int band_w = 0;            // PSE_BAND_W: 16 or 32 (0: chosen per run)
   int64_t layer_pairs = 0;   // average conv layer size in coefficient pairs
 
   // First conv layer the banded path runs for this batch (layer_rows.size():
@@ -468,15 +490,34 @@ struct Plan {
       bw.jobs = dev_upload(v, stream);
     }
     const int warps = sms * L->band_blocks_per_sm(flow()) * (kLaneThreads / 32);
-    const int64_t cap2 = std::max<int64_t>(2, static_cast<int64_t>(2 * band_rounds * warps / batch));
-    const BandSched sch = band_schedule(rows, d, cap2, flow(), std::max(1, warps / batch), flow_slack);
+    const int64_t cap_slots = std::max<int64_t>(kSlots, static_cast<int64_t>(kSlots * band_rounds * warps / batch));
+    // per-task fixed cost in steps: ~4 us of hand-out / flags / partial sums
+    // against one md_mul + md_add (instrumented ops; ~2000 ops per us-warp)
+    const Costs cst = costs(m);
+    const double ovh = 2000.0 / static_cast<double>(cst.inst_mul + cst.inst_add);
+    auto sched = [&](int W) {
+      return band_schedule(rows, d, W, cap_slots, flow(), std::max(1, warps / batch) * (32 / W), flow_slack, ovh);
+    };
+    // Band width: 16 halves the dependency chain of a deep graph (dataflow
+    // critical path), 32 halves the number of tasks; in flow mode the one
+    // with the shorter simulated makespan wins unless PSE_BAND_W fixes it.
+    BandSched sch;
+    if (band_w || !flow()) {
+      bw.W = band_w ? band_w : 32;
+      sch = sched(bw.W);
+    } else {
+      BandSched s16 = sched(16), s32 = sched(32);
+      const bool narrow = s16.makespan < s32.makespan;
+      bw.W = narrow ? 16 : 32;
+      sch = std::move(narrow ? s16 : s32);
+    }
     std::vector<int4> all;
     for (auto& w : sch.waves) {
-      bw.waves.emplace_back(static_cast<int64_t>(all.size()), static_cast<int>(w.size()));
+      bw.waves.emplace_back(static_cast<int64_t>(all.size() / kSlots), static_cast<int>(w.size() / kSlots));
       all.insert(all.end(), w.begin(), w.end());
     }
     bw.tasks = dev_upload(all, stream);
-    bw.nunits = static_cast<int>(all.size());
+    bw.nunits = static_cast<int>(all.size() / kSlots);
     if (flow()) {
       bw.dep_off = dev_upload(sch.dep_off, stream);
       bw.deps = dev_upload(sch.deps, stream);
@@ -578,12 +619,12 @@ struct Plan {
       if (flow()) {
         ck(cudaMemsetAsync(flow_flags, 0, sizeof(unsigned) * batch * bw.nunits, stream), "flags");
         ck(cudaMemsetAsync(flow_counter, 0, sizeof(unsigned long long), stream), "counter");
-        FlowArgs a{arena, G, bw.jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, flow_flags, flow_counter};
+        FlowArgs a{arena, G, bw.jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, flow_flags, flow_counter, bw.W};
         L->conv_flow(a, sms * L->band_blocks_per_sm(true), stream);
         ++launches;
       } else {
         for (auto& [o, nw] : bw.waves) {
-          BandArgs a{arena, G, bw.jobs, bw.tasks + o, nw, batch};
+          BandArgs a{arena, G, bw.jobs, bw.tasks + o * kSlots, nw, batch, bw.W};
           L->conv_band(a, stream);
           ++launches;
         }
@@ -824,6 +865,8 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
       if (br && atof(br) > 0) p->band_rounds = atof(br);
       const char* fs = getenv("PSE_FLOW_SLACK");
       if (fs && atof(fs) >= 0) p->flow_slack = atof(fs);
+      const char* bwv = getenv("PSE_BAND_W");
+      if (bwv && (atoi(bwv) == 16 || atoi(bwv) == 32)) p->band_w = atoi(bwv);
     }
     // exchange lists: every dynamic slot the addition stage, the term scales
     // or the extraction reads, by the rank whose conv jobs produce it

@@ -87,48 +87,52 @@ struct SplitArgs {
 };
 
 // Banded convolution (deep graphs, few jobs per layer). A conv job's output
-// coefficients are cut into bands -- band 0 = [0, W0) with W0 = d % kBandW + 1,
-// then full bands of kBandW, so that every rectangular task fills a warp --
-// and the accumulation chain of a coefficient k (steps i = 0..k, ascending)
-// into segments at the same boundaries.
+// coefficients are cut into bands of width W (16 or 32) -- band 0 = [0, W0)
+// with W0 = d % W + 1, then full bands, so that every rectangular task has W
+// busy lanes -- and the accumulation chain of a coefficient k (steps
+// i = 0..k, ascending) into segments at the same boundaries.
 // A task (job, band b, segment s <= b) runs the steps i in segment s of the
 // chains of every k in band b; the running sum is carried between segments
 // in the output slot itself (exact binary64 words), so the operation order of
 // conv() is unchanged and the result is bit-identical. A task needs only
 // band s of in1 and bands <= b-s of in2, so a job's low bands finish -- and
 // unlock the next layer -- while its high bands still accumulate: the host
-// schedules tasks into waves (one launch each) over that dependency graph.
-// One warp per task descriptor (int4 {job, k0, i0, aux}):
-//   aux == -1  rectangular task (s < b): lane l owns k = k0 + l, the steps
-//              i of segment s (all < k0 <= k);
-//   aux >= 0 or -2  diagonal tasks (s == b) of two jobs (x = job, aux =
-//              second job or -2 for none), one per half-warp: lane j owns
-//              k = k0+j and k = k0+width-1-j, steps k0..k -- width+1 steps
-//              per lane, balanced;
-//   aux == -3  copy job, band k0: out := in1 on coefficients k0 + lane.
-constexpr int kBandW = 32;
+// schedules tasks over that dependency graph.
+// A warp descriptor is kSlots int4 slots of 8 lanes each; a task fills W/8
+// (rectangular, copy) or W/16 (diagonal) aligned slots, each holding the
+// task as {job, k0 = first coefficient of the band, i0 = first step, kind}:
+//   kind -1  rectangular task (s < b): lane t of the task owns k = k0 + t,
+//            the steps i of segment s (all < k0 <= k);
+//   kind -2  diagonal task (s == b), W/2 lanes: lane j owns k = k0+j and
+//            k = k0+width-1-j, steps k0..k -- width+1 steps per lane;
+//   kind -3  copy job, band k0: out := in1 on coefficients k0 + t;
+//   kind -4  empty slot.
+constexpr int kBandW = 32;  // widest band
+constexpr int kSlots = 4;   // 8-lane slots per warp descriptor
 
 struct BandArgs {
   double* arena;
   Geom G;
   const int4* jobs;   // (in1, in2, out, flags) of every banded conv job;
                       // flags: 2 = in1 and 4 = in2 produced by a conv job
-  const int4* tasks;  // warp descriptors of one wave
-  int ntasks;
+  const int4* tasks;  // kSlots slots per warp descriptor, one wave
+  int ntasks;         // warp descriptors
   int batch;
+  int W;              // band width
 };
 
 struct FlowArgs {
   double* arena;
   Geom G;
   const int4* jobs;     // as BandArgs
-  const int4* tasks;    // every descriptor, in scheduled order
+  const int4* tasks;    // kSlots slots per warp descriptor, in scheduled order
   const int* dep_off;   // [nunits+1] CSR of the descriptors each one waits for
   const int* deps;
   int nunits;
   int batch;
   unsigned* flags;      // [batch][nunits], zero before the launch
   unsigned long long* counter;  // zero before the launch
+  int W;                // band width
 };
 
 struct Launchers {
@@ -301,71 +305,81 @@ __global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
 // the job's .w) may have been written during this kernel by other SMs and
 // are read through L2; static inputs keep the read-only path.
 // Dataflow tasks of short steps (M <= 4) stage their operand windows in
-// shared memory first -- the in1 segment (<= kBandW words per limb) and the
-// in2 range the task reads (<= 2*kBandW) -- so a task pays one L2 round trip
-// instead of one per step. kStageSlots words per limb and warp: rectangular
-// tasks use x [0,32) and y [32,96); diagonal half-warp h uses x [64h, 64h+32)
-// and y [64h+32, 64h+64).
+// shared memory first -- the in1 segment (<= W words per limb) and the in2
+// range the task reads (<= 2W) -- so a task pays one L2 round trip instead
+// of one per step. kStageSlots words per limb and warp: the task whose first
+// slot is f uses words [32f, 32f + 3W) (x first, then y).
 constexpr int kStageSlots = 128;
 template <int M, bool COH>
 __host__ __device__ constexpr bool band_stage() {
   return COH && M <= 4;
 }
 
+// lanes of a task of kind `kind` (band width W)
+__device__ __forceinline__ int band_task_lanes(int kind, int W) { return kind == -2 ? W / 2 : W; }
+
 template <int M, bool CPLX, bool COH>
-__device__ __forceinline__ void band_task(double* arena, const Geom& G, const int4* __restrict__ jobs, const int4 T,
-                                          int64_t pt, int lane, Lane sm, double* __restrict__ stg) {
+__device__ __forceinline__ void band_task(double* arena, const Geom& G, const int4* __restrict__ jobs,
+                                          const int4* __restrict__ slots, int W, int64_t pt, int lane, Lane sm,
+                                          double* __restrict__ stg) {
   const int S = G.S, d = G.d;
   constexpr int Q = CPLX ? 2 * M : M;
   constexpr bool STAGE = band_stage<M, COH>();
   double* base = arena + pt * G.point_words;
-  // band 0 is [0, W0) with W0 = d % kBandW + 1, the others are full
-  const int W0 = d % kBandW + 1;
-  const int width = T.y == 0 ? W0 : kBandW;
-  const bool diag = T.w != -1 && T.w != -3;
-  // staged windows: x_i at slot xo + i - xb, y_j at slot yo + j - yb
+  // band 0 is [0, W0) with W0 = d % W + 1, the others are full
+  const int W0 = d % W + 1;
+  const int4 T = slots[lane >> 3];
+  const int kind = T.w;
+  const int span = band_task_lanes(kind, W);
+  const int lt = lane & (span - 1);  // lane within the task
+  const int width = T.y == 0 ? W0 : W;
+  // staged windows: x_i at word xo + i - xb, y_j at word yo + j - yb
   int xb = 0, yb = 0, xo = 0, yo = 0;
   if constexpr (STAGE) {
-    if (T.w != -3) {
-      const int ws = T.z == 0 ? W0 : kBandW;  // segment width (rectangular)
 #pragma unroll 1
-      for (int h = 0; h < (diag ? 2 : 1); ++h) {
-        const int jh = h ? T.w : T.x;
-        if (jh < 0) continue;
-        const int4 Jh = jobs[jh];
-        const double* Xh = base + static_cast<int64_t>(Jh.x) * G.slot_words;
-        const double* Yh = base + static_cast<int64_t>(Jh.y) * G.slot_words;
-        const bool chx = COH && (Jh.w & 2), chy = COH && (Jh.w & 4);
-        const int hxb = diag ? T.y : T.z, hyb = diag ? 0 : T.y - T.z - ws + 1;
-        const int hxo = diag ? 64 * h : 0, hyo = hxo + 32, ny = diag ? 1 : 2;
+    for (int f = 0; f < kSlots; ++f) {
+      const int4 Tf = slots[f];
+      if (Tf.w == -4 || Tf.w == -3 || (f & (band_task_lanes(Tf.w, W) / 8 - 1)) != 0) continue;
+      const bool dg = Tf.w == -2;
+      const int ws = Tf.z == 0 ? W0 : W;  // segment width (rectangular)
+      const int4 Jh = jobs[Tf.x];
+      const double* Xh = base + static_cast<int64_t>(Jh.x) * G.slot_words;
+      const double* Yh = base + static_cast<int64_t>(Jh.y) * G.slot_words;
+      const bool chx = COH && (Jh.w & 2), chy = COH && (Jh.w & 4);
+      const int hxb = dg ? Tf.y : Tf.z, hyb = dg ? 0 : Tf.y - Tf.z - ws + 1;
+      const int hxo = 32 * f, hyo = hxo + W, ny = dg ? W : 2 * W;
 #pragma unroll 1
-        for (int q = 0; q < Q; ++q) {
-          const int ix = hxb + lane;
-          if (ix <= d) stg[q * kStageSlots + hxo + lane] = chx ? __ldcg(Xh + q * S + ix) : __ldg(Xh + q * S + ix);
-          for (int r = 0; r < ny; ++r) {
-            const int iy = hyb + 32 * r + lane;
-            if (iy >= 0 && iy <= d)
-              stg[q * kStageSlots + hyo + 32 * r + lane] = chy ? __ldcg(Yh + q * S + iy) : __ldg(Yh + q * S + iy);
-          }
+      for (int q = 0; q < Q; ++q) {
+        for (int e = lane; e < W; e += 32) {
+          const int ix = hxb + e;
+          if (ix <= d) stg[q * kStageSlots + hxo + e] = chx ? __ldcg(Xh + q * S + ix) : __ldg(Xh + q * S + ix);
+        }
+        for (int e = lane; e < ny; e += 32) {
+          const int iy = hyb + e;
+          if (iy >= 0 && iy <= d) stg[q * kStageSlots + hyo + e] = chy ? __ldcg(Yh + q * S + iy) : __ldg(Yh + q * S + iy);
         }
       }
-      const int h = diag ? lane >> 4 : 0;
-      xb = diag ? T.y : T.z;
-      yb = diag ? 0 : T.y - T.z - ws + 1;
-      xo = diag ? 64 * h : 0;
-      yo = xo + 32;
+    }
+    if (kind != -4 && kind != -3) {
+      const int f0 = (lane >> 3) & ~(span / 8 - 1);  // first slot of this lane's task
+      const int ws = T.z == 0 ? W0 : W;
+      xb = kind == -2 ? T.y : T.z;
+      yb = kind == -2 ? 0 : T.y - T.z - ws + 1;
+      xo = 32 * f0;
+      yo = xo + W;
     }
     __syncwarp();
   }
-  int job = T.x, kA, iaA, ibA, kB = -1, iaB = 0, ibB = -1;
-  if (!diag) {
-    if (lane >= width) return;
-    kA = T.y + lane;
+  if (kind == -4) return;
+  const int job = T.x;
+  int kA, iaA, ibA, kB = -1, iaB = 0, ibB = -1;
+  if (kind != -2) {
+    if (lt >= width) return;
+    kA = T.y + lt;
     iaA = T.z;
-    ibA = (T.z == 0 ? W0 : T.z + kBandW) - 1;
+    ibA = (T.z == 0 ? W0 : T.z + W) - 1;
   } else {
-    if (lane >= 16) job = T.w;
-    const int j = lane & 15;
+    const int j = lt;
     if (2 * j >= width) return;
     kA = T.y + j;
     iaA = T.y;
@@ -375,13 +389,13 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
     ibB = kB;
     if (kB == kA) kB = -1;
   }
-  if (job < 0 || kA > d) return;
+  if (kA > d) return;
   const int4 J = jobs[job];
   const double* __restrict__ X = base + static_cast<int64_t>(J.x) * G.slot_words;
   const double* __restrict__ Y = base + static_cast<int64_t>(J.y) * G.slot_words;
   double* Z = base + static_cast<int64_t>(J.z) * G.slot_words;
   const bool cx = COH && (J.w & 2), cy = COH && (J.w & 4);
-  if (T.w == -3) {  // copy job (executor.cpp:130-133)
+  if (kind == -3) {  // copy job (executor.cpp:130-133)
 #pragma unroll 1
     for (int q = 0; q < Q; ++q) Z[q * S + kA] = cx ? __ldcg(X + q * S + kA) : X[q * S + kA];
     return;
@@ -479,7 +493,8 @@ __global__ void __launch_bounds__(kConvThreads, 4) k_conv_band(const BandArgs a)
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (gw >= static_cast<int64_t>(a.batch) * a.ntasks) return;
   const int tw = static_cast<int>(gw % a.ntasks);
-  band_task<M, CPLX, false>(a.arena, a.G, a.jobs, a.tasks[tw], gw / a.ntasks, threadIdx.x & 31, sm, nullptr);
+  band_task<M, CPLX, false>(a.arena, a.G, a.jobs, a.tasks + static_cast<int64_t>(tw) * kSlots, a.W, gw / a.ntasks,
+                            threadIdx.x & 31, sm, nullptr);
 }
 
 // Dataflow form of the banded convolution: ONE persistent launch. Warps take
@@ -525,7 +540,7 @@ __global__ void __launch_bounds__(kConvThreads, 4) k_conv_flow(const FlowArgs a)
       }
     }
     __syncwarp();
-    band_task<M, CPLX, true>(a.arena, a.G, a.jobs, a.tasks[p], pt, lane, sm, stg);
+    band_task<M, CPLX, true>(a.arena, a.G, a.jobs, a.tasks + static_cast<int64_t>(p) * kSlots, a.W, pt, lane, sm, stg);
     __syncwarp();  // the staging area is rewritten by the next unit
     __threadfence();
     __syncwarp();

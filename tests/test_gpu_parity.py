@@ -18,18 +18,21 @@ pytestmark = pytest.mark.gpu
 LEVELS = [1, 2, 3, 4, 5, 8, 10]
 
 
-@pytest.fixture(params=["fused", "split", "band", "flow"])
+@pytest.fixture(params=["fused", "split", "band", "flow", "flow32"])
 def conv_path(request, monkeypatch):
     """Run an engine test through the fused conv kernel (one thread per
     coefficient pair), through the split path (products in parallel, then
     the accumulation chains), through the banded wavefront (chains cut into
     band x segment tasks, scheduled across layers, one launch per wave) and
     through its dataflow form (one persistent launch, per-task completion
-    flags). The planner reads
+    flags; 16- and 32-wide bands). The planner reads
     PSE_CONV_MODE and PSE_SPLIT_THRESHOLD when a plan is created: 0 forces
     fused, a huge value forces split."""
-    if request.param in ("band", "flow"):
-        monkeypatch.setenv("PSE_CONV_MODE", request.param)
+    if request.param in ("band", "flow", "flow32"):
+        # waves use 32-wide bands, the dataflow kernel 16 (flow32: 32)
+        monkeypatch.setenv("PSE_CONV_MODE", request.param[:4])
+        if request.param == "flow32":
+            monkeypatch.setenv("PSE_BAND_W", "32")
     else:
         monkeypatch.setenv("PSE_CONV_MODE", "layer")
         monkeypatch.setenv("PSE_SPLIT_THRESHOLD", "0" if request.param == "fused" else str(1 << 60))
