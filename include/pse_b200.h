@@ -198,6 +198,13 @@ int pse_plan_stream(const pse_plan* p, void** stream);
  * for the trailing small ones) */
 enum { PSE_CONV_LAYERED = 1, PSE_CONV_WAVES = 2, PSE_CONV_DATAFLOW = 3, PSE_CONV_HYBRID = 4 };
 int pse_plan_conv_path(const pse_plan* p, int32_t batch, int32_t* path);
+/* host only (no device): the banded task schedule of a whole graph with band
+ * width W (16 or 32), in dataflow order (flow != 0) or waves of `procs` warps;
+ * the scheduler checks that every descriptor's dependencies precede it.
+ * out[7] = {conv jobs, tasks, warp descriptors, waves, dependency entries,
+ * occupied 8-lane slots, makespan estimate in steps} */
+int pse_band_schedule_stats(const pse_graph_desc* desc, int32_t W, int32_t flow, int64_t procs, double slack,
+                            int64_t* out);
 
 /* evaluate() (executor.cpp:271-276): build graph, fold exponents (on the
  * device), stage, run, extract, for `batch` points sharing one polynomial

@@ -141,6 +141,43 @@ T* dev_upload(const std::vector<T>& v, cudaStream_t s) {
   return p;
 }
 
+// Conv rows per layer (prologue layers first, then the graph's), with
+// in-place jobs (out == in1, the coefficient fold b := b * a,
+// jobgraph.cpp:115) made out-of-place: the earlier job that produced the
+// pre-fold value writes a fresh slot (*next_slot++) that the fold and every
+// reader in between read instead.
+std::vector<std::vector<ConvRow>> versioned_layers(const pse_graph_desc& g,
+                                                   const std::vector<std::vector<ConvRow>>& prologue,
+                                                   int64_t* next_slot) {
+  std::vector<std::vector<ConvRow>> layers = prologue;
+  for (int32_t L = 0; L < g.n_conv_layers; ++L) {
+    std::vector<ConvRow> rows;
+    for (int64_t t = g.conv_layer_off[L]; t < g.conv_layer_off[L + 1]; ++t)
+      rows.push_back({g.conv_in1[t], g.conv_in2[t], g.conv_out[t], g.conv_copy[t]});
+    layers.push_back(std::move(rows));
+  }
+  std::map<int64_t, std::pair<size_t, size_t>> last_writer;  // slot -> (layer, row)
+  for (size_t L = 0; L < layers.size(); ++L) {
+    for (size_t r = 0; r < layers[L].size(); ++r) {
+      ConvRow& j = layers[L][r];
+      if (j.copy || j.out != j.in1) continue;
+      auto it = last_writer.find(j.in1);
+      if (it == last_writer.end()) throw std::invalid_argument("in-place job on a slot without an earlier writer");
+      const int64_t s = j.in1, scratch = (*next_slot)++;
+      const size_t Lw = it->second.first;
+      layers[Lw][it->second.second].out = scratch;
+      for (size_t L2 = Lw + 1; L2 <= L; ++L2)
+        for (ConvRow& q : layers[L2]) {
+          if (&q != &j && q.out == s && L2 < L) throw std::invalid_argument("slot rewritten before in-place use");
+          if (q.in1 == s) q.in1 = scratch;
+          if (!q.copy && q.in2 == s) q.in2 = scratch;
+        }
+    }
+    for (size_t r = 0; r < layers[L].size(); ++r) last_writer[layers[L][r].out] = {L, r};
+  }
+  return layers;
+}
+
 // Banded conv schedule (see BandArgs in kernels.cuh), band width W. Tasks
 // (job, band b, segment s <= b) -- one per band for copy jobs -- with the
 // dependencies:
@@ -720,36 +757,9 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
   p->L->prepare();
 
   // conv rows per layer: prologue layers first, then the graph's layers
-  std::vector<std::vector<ConvRow>> layers = prologue;
-  for (int32_t L = 0; L < g.n_conv_layers; ++L) {
-    std::vector<ConvRow> rows;
-    for (int64_t t = g.conv_layer_off[L]; t < g.conv_layer_off[L + 1]; ++t) {
-      rows.push_back({g.conv_in1[t], g.conv_in2[t], g.conv_out[t], g.conv_copy[t]});
-      if (g.conv_copy[t]) ++p->copy_jobs;
-    }
-    layers.push_back(std::move(rows));
-  }
   int64_t next_slot = g.total_slots + prologue_slots;
-  // version in-place slots (out == in1, not a copy)
-  std::map<int64_t, std::pair<size_t, size_t>> last_writer;  // slot -> (layer, row)
-  for (size_t L = 0; L < layers.size(); ++L) {
-    for (size_t r = 0; r < layers[L].size(); ++r) {
-      ConvRow& j = layers[L][r];
-      if (j.copy || j.out != j.in1) continue;
-      auto it = last_writer.find(j.in1);
-      if (it == last_writer.end()) throw std::invalid_argument("in-place job on a slot without an earlier writer");
-      const int64_t s = j.in1, scratch = next_slot++;
-      const size_t Lw = it->second.first;
-      layers[Lw][it->second.second].out = scratch;
-      for (size_t L2 = Lw + 1; L2 <= L; ++L2)
-        for (ConvRow& q : layers[L2]) {
-          if (&q != &j && q.out == s && L2 < L) throw std::invalid_argument("slot rewritten before in-place use");
-          if (q.in1 == s) q.in1 = scratch;
-          if (!q.copy && q.in2 == s) q.in2 = scratch;
-        }
-    }
-    for (size_t r = 0; r < layers[L].size(); ++r) last_writer[layers[L][r].out] = {L, r};
-  }
+  std::vector<std::vector<ConvRow>> layers = versioned_layers(g, prologue, &next_slot);
+  for (int64_t t = 0; t < g.conv_layer_off[g.n_conv_layers]; ++t) p->copy_jobs += g.conv_copy[t] ? 1 : 0;
   p->TSdev = next_slot;
   p->G.d = g.d;
   p->G.S = (g.d + 1 + 3) / 4 * 4;
@@ -1333,6 +1343,41 @@ int pse_plan_conv_path(const pse_plan* p, int32_t batch, int32_t* path) {
           : P.band_first(batch) > 0 ? PSE_CONV_HYBRID
                                     : PSE_CONV_DATAFLOW;
   return PSE_OK;
+}
+
+int pse_band_schedule_stats(const pse_graph_desc* desc, int32_t W, int32_t flow, int64_t procs, double slack,
+                            int64_t* out) {
+  return pse::guarded([&] {
+    if (!desc || !out) throw std::invalid_argument("null argument");
+    if (W != 16 && W != 32) throw std::invalid_argument("band width must be 16 or 32");
+    if (procs < 1) throw std::invalid_argument("procs must be at least 1");
+    const std::string why = pse::validate_desc(*desc);
+    if (!why.empty()) throw std::invalid_argument("invalid job graph: " + why);
+    int64_t next = desc->total_slots;
+    const auto layers = pse::versioned_layers(*desc, {}, &next);
+    std::vector<pse::ConvRow> rows;
+    for (auto& l : layers) rows.insert(rows.end(), l.begin(), l.end());
+    const pse::BandSched s = pse::band_schedule(rows, desc->d, W, pse::kSlots * procs, flow != 0, procs * (32 / W),
+                                                slack, 1.0);
+    int64_t descs = 0, tasks = 0, slots = 0;
+    for (auto& w : s.waves) {
+      descs += static_cast<int64_t>(w.size()) / pse::kSlots;
+      for (size_t i = 0; i < w.size(); ++i) {
+        if (w[i].w == -4) continue;
+        ++slots;
+        const int lanes = w[i].w == -2 ? W / 2 : W;
+        if (static_cast<int>(i % pse::kSlots) % (lanes / 8) == 0) ++tasks;  // first slot of a task
+      }
+    }
+    out[0] = static_cast<int64_t>(rows.size());
+    out[1] = tasks;
+    out[2] = descs;
+    out[3] = static_cast<int64_t>(s.waves.size());
+    out[4] = static_cast<int64_t>(s.deps.size());
+    out[5] = slots;
+    out[6] = static_cast<int64_t>(s.makespan);
+    return PSE_OK;
+  });
 }
 
 int pse_plan_info(const pse_plan* p, int64_t* out) {

@@ -223,6 +223,17 @@ class GraphArrays:
         return d
 
 
+def band_schedule_stats(g, W: int, flow: bool = True, procs: int = 2368, slack: float = 0.3) -> dict:
+    """The banded conv schedule of graph g (host only, pse_band_schedule_stats):
+    task and descriptor counts of the dataflow order (flow) or of waves of
+    `procs` warps; raises if a descriptor would wait on a later one."""
+    out = np.zeros(7, np.int64)
+    d = g.desc(1, REAL)
+    check(lib().pse_band_schedule_stats(C.byref(d), W, int(flow), procs, slack, out.ctypes.data))
+    keys = ("jobs", "tasks", "descriptors", "waves", "dep_entries", "slots", "makespan_steps")
+    return dict(zip(keys, (int(v) for v in out)))
+
+
 def build_jobgraph_shape(n: int, d: int, nvars, indices, exponents=None) -> JobGraph:
     nv = np.ascontiguousarray(nvars, np.int32)
     ix = np.ascontiguousarray(indices, np.int32)
