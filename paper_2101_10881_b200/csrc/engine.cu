@@ -487,7 +487,7 @@ struct Plan {
   std::map<int, BandWaves> band_waves;
   int conv_mode = 0;         // PSE_CONV_MODE: 0 auto, 1 layered, 2 banded waves, 3 dataflow
   double band_rounds = 1.0;  // PSE_BAND_ROUNDS: wave size in resident warps
-  double flow_slack = 0.3;   // PSE_FLOW_SLACK: see band_schedule
+  double flow_slack = 1.0;   // PSE_FLOW_SLACK: see band_schedule (swept: 0.1-8, best 1)
   int band_w = 0;            // PSE_BAND_W: 16 or 32 (0: chosen per run)
   int64_t layer_pairs = 0;   // average conv layer size in coefficient pairs
 
