@@ -230,6 +230,37 @@ def test_errors_are_invalid_argument():
         pe.evaluate_packed(2, 3, 2, "real", [2], [2, 1], None, np.zeros((2, 1, 4, 4)))
 
 
+def _p2h(p: po.Problem) -> po.Problem:
+    """C3': p2's even cyclic windows (bench.py make_static)."""
+    keep = np.arange(0, p.N, 2)
+    starts = np.concatenate([[0], np.cumsum(p.nvars)])
+    idx = np.concatenate([p.idx[starts[k]:starts[k + 1]] for k in keep]).astype(np.int32)
+    stat = np.concatenate([p.stat[:, :, :1], p.stat[:, :, 1 + keep], p.stat[:, :, 1 + p.N:]], axis=2)
+    return po.Problem(p.n, p.d, p.m, p.cplx, p.nvars[keep].copy(), idx, None, np.ascontiguousarray(stat), "p2h")
+
+
+@pytest.mark.parametrize("cfg,pid,m", [("C2", "p1", 10), ("C3", "p2", 10), ("C3'", "p2h", 10), ("C4", "p3", 10),
+                                       ("C3 m=2", "p2", 2), ("C3 m=5", "p2", 5)])
+def test_benchmark_configs_full_size_bitwise_vs_reference_engine(cfg, pid, m):
+    """The BASELINE configurations at full size (d=152, seed 7) through the
+    conv path the planner picks for them (layered/hybrid for C2 and C4,
+    dataflow for C3 and C3'): value and every gradient series equal the
+    reference engine's run_parallel (oracle/_ref, the reference's own
+    sources) bit for bit."""
+    import os
+
+    if not po.has_ref():
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    p = po.gen_benchmark("p2" if pid == "p2h" else pid, 152, m, seed=7)
+    if pid == "p2h":
+        p = _p2h(p)
+    ref = po.evaluate(p, "ref", workers=os.cpu_count() or 1)
+    g = pe.build_jobgraph_shape(p.n, p.d, p.nvars, p.idx)
+    plan = pe.DevicePlan(g, m, "real", 0, 1)
+    vg, _, rep = plan.run(p.stat.reshape(p.P * m, *p.stat.shape[2:]), 1)
+    assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"{cfg}: {pid} d=152 m={m} ({plan.conv_path(1)})")
+
+
 def test_reference_binding_drop_in():
     """include/pse_b200_pseval.hpp compiled against the unmodified reference
     sources: run_device == run_sequential bit for bit on the reference's own
