@@ -301,9 +301,9 @@ __global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
 // coefficient pair. A piece that starts past i = 0 resumes from the partial
 // sum its job's previous segment stored in Z[k]; every piece ends by storing
 // its sum there (final once i reaches k).
-// COH (dataflow kernel): inputs produced by conv jobs (flag bits 1 and 2 of
-// the job's .w) may have been written during this kernel by other SMs and
-// are read through L2; static inputs keep the read-only path.
+// COH (dataflow kernel): inputs produced inside the launch (flag bits 2 =
+// in1 and 4 = in2 of the job's .w) may have been written by other SMs during
+// it and are read through L2; other inputs keep the read-only path.
 // Dataflow tasks of short steps (M <= 4) stage their operand windows in
 // shared memory first -- the in1 segment (<= W words per limb) and the in2
 // range the task reads (<= 2W) -- so a task pays one L2 round trip instead
