@@ -241,6 +241,7 @@ def ours(args, wl):
     model_ops = pe.flop_count(g, d, "real", pe.reporting_cost(m))
     conv_ops = conv_alg_ops(g, d, m)
     peak = pe.fp64_peak(dev)
+    sms_count = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_ops = max(peak["dadd"], peak["dfma"])
 
     # L2 flush buffer (> 126 MB L2), written between timed steps
@@ -349,7 +350,9 @@ def ours(args, wl):
             "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s (binary64, algorithmic)",
             "frac": achieved / peak_ops, "traffic": load_traffic(wl, path),
             "traffic_unit": "DRAM bytes of the conv stage per evaluation point (ncu, profiles/ncu_traffic.json)",
-            "peak_source": "measured live: pse_fp64_peak (independent DADD/DFMA chains on every SM)",
+            "peak_source": "measured live: pse_fp64_peak (independent DADD/DFMA chains on every SM, best of two shapes)",
+            "peak_nominal": sms_count * 64 * (clk.summary().get("sm_max_mhz") or 0) * 1e6 / 1e12,
+            "peak_nominal_note": "SMs x 64 FP64 lanes x max SM clock (binary64 instructions/s)",
             "conv_ms_per_eval": conv_ms / (len(mine) * args.steps),
             "alg_ops_per_eval": conv_ops,
         },

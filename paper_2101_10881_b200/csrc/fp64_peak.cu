@@ -2,8 +2,12 @@
 // convolution kernels (the peak must be measured on the box;
 // MEASURED_PEAKS.json carries only HBM and bf16 tensor figures).
 //
-// Each thread runs 8 independent dependency chains of DADD (or DFMA) so the
-// FP64 pipe, not latency, is the limit; the grid fills every SM.
+// Each thread runs CH independent dependency chains of DADD (or DFMA) so the
+// FP64 pipe, not latency, is the limit; the grid fills every SM. Two shapes
+// are timed (16 chains x 4 blocks/SM, 32 chains x 2 blocks/SM, ~2 ms each)
+// and the best rate is the peak: with 8 chains x 8 blocks/SM the same
+// kernel stays ~4% below (17.0 vs 17.8 T lane-ops/s at 1965 MHz, where
+// 148 SMs x 64 lanes give 18.6 T).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -13,10 +17,9 @@
 namespace pse {
 namespace {
 
-constexpr int kChains = 8;
-constexpr int kIters = 4096;
+constexpr int kIters = 16384;
 
-template <bool FMA>
+template <bool FMA, int kChains>
 __global__ void __launch_bounds__(256) k_fp64_peak(double* sink, double seed) {
   double a[kChains];
 #pragma unroll
@@ -57,27 +60,30 @@ int pse_fp64_peak(int32_t device, double* out) {
     pse::set_error("cudaMalloc failed");
     return PSE_ECUDA;
   }
-  const int blocks = sms * 8;
+  int blocks = 0;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   double rate[2] = {0, 0};
   float last = 0;
-  for (int f = 0; f < 2; ++f) {
-    for (int rep = 0; rep < 4; ++rep) {  // warm-up + best of 3
-      cudaEventRecord(e0);
-      if (f)
-        pse::k_fp64_peak<true><<<blocks, 256>>>(sink, 1.0);
-      else
-        pse::k_fp64_peak<false><<<blocks, 256>>>(sink, 1.0);
-      cudaEventRecord(e1);
-      cudaEventSynchronize(e1);
-      float ms = 0;
-      cudaEventElapsedTime(&ms, e0, e1);
-      const double ops = double(blocks) * 256 * pse::kChains * pse::kIters;
-      if (rep > 0 && ops / (ms * 1e-3) > rate[f]) {
-        rate[f] = ops / (ms * 1e-3);
-        if (!f) last = ms;
+  for (int shape = 0; shape < 2; ++shape) {
+    const int chains = shape ? 32 : 16, nb = sms * (shape ? 2 : 4);
+    for (int f = 0; f < 2; ++f) {
+      for (int rep = 0; rep < 3; ++rep) {  // warm-up + best of 2
+        cudaEventRecord(e0);
+        if (shape == 0 && f) pse::k_fp64_peak<true, 16><<<nb, 256>>>(sink, 1.0);
+        if (shape == 0 && !f) pse::k_fp64_peak<false, 16><<<nb, 256>>>(sink, 1.0);
+        if (shape == 1 && f) pse::k_fp64_peak<true, 32><<<nb, 256>>>(sink, 1.0);
+        if (shape == 1 && !f) pse::k_fp64_peak<false, 32><<<nb, 256>>>(sink, 1.0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double ops = double(nb) * 256 * chains * pse::kIters;
+        if (rep > 0 && ops / (ms * 1e-3) > rate[f]) {
+          rate[f] = ops / (ms * 1e-3);
+          if (!f) last = ms, blocks = nb;
+        }
       }
     }
   }
