@@ -464,7 +464,15 @@ def main():
     ap.add_argument("--points", type=int, default=0,
                     help="override the workload's point count (per GPU for C1-C4, total for C5)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--m", type=int, default=0, choices=[0, 1, 2, 3, 4, 5, 8, 10],
+                    help="override the precision level (C3's sweep: 1/2/3/4/5/8/10)")
     args = ap.parse_args()
+    if args.m:
+        pid, d, m, ppg, desc = WORKLOADS[args.workload]
+        names = {1: "double", 2: "double-double", 3: "triple double", 4: "quad double", 5: "penta double",
+                 8: "octo double", 10: "deca double"}
+        WORKLOADS[args.workload] = (pid, d, args.m, ppg, desc.replace("deca double", names[args.m]).replace(
+            "d=152", f"d=152, m={args.m}") if args.m != m else desc)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
