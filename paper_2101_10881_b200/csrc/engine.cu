@@ -489,6 +489,7 @@ struct Plan {
   double band_rounds = 1.0;  // PSE_BAND_ROUNDS: wave size in resident warps
   double flow_slack = 1.0;   // PSE_FLOW_SLACK: see band_schedule (swept: 0.1-8, best 1)
   int band_w = 0;            // PSE_BAND_W: 16 or 32 (0: chosen per run)
+  double flow_procs = 1.0;   // PSE_FLOW_PROCS: simulated warps, as a fraction of the resident ones
   int64_t layer_pairs = 0;   // average conv layer size in coefficient pairs
 
   // First conv layer the banded path runs for this batch (layer_rows.size():
@@ -533,7 +534,8 @@ struct Plan {
     const Costs cst = costs(m);
     const double ovh = 2000.0 / static_cast<double>(cst.inst_mul + cst.inst_add);
     auto sched = [&](int W) {
-      return band_schedule(rows, d, W, cap_slots, flow(), std::max(1, warps / batch) * (32 / W), flow_slack, ovh);
+      const int64_t procs = std::max<int64_t>(1, static_cast<int64_t>(flow_procs * warps / batch)) * (32 / W);
+      return band_schedule(rows, d, W, cap_slots, flow(), procs, flow_slack, ovh);
     };
     // Band width: 16 halves the dependency chain of a deep graph (dataflow
     // critical path), 32 halves the number of tasks; in flow mode the one
@@ -875,6 +877,8 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
       if (br && atof(br) > 0) p->band_rounds = atof(br);
       const char* fs = getenv("PSE_FLOW_SLACK");
       if (fs && atof(fs) >= 0) p->flow_slack = atof(fs);
+      const char* fp = getenv("PSE_FLOW_PROCS");
+      if (fp && atof(fp) > 0) p->flow_procs = atof(fp);
       const char* bwv = getenv("PSE_BAND_W");
       if (bwv && (atoi(bwv) == 16 || atoi(bwv) == 32)) p->band_w = atoi(bwv);
     }

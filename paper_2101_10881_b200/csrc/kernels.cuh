@@ -500,15 +500,16 @@ __global__ void __launch_bounds__(kConvThreads, 4) k_conv_band(const BandArgs a)
 // Dataflow form of the banded convolution: ONE persistent launch. Warps take
 // work units (descriptor p of the scheduled order, point b) from a global
 // counter in order, wait until the units p depends on are done for point b
-// (acquire loads of their flags), run the task and publish their own flag
+// (relaxed polls of their flags + an acquire fence), run the task and publish their own flag
 // (stores, fence, release). A unit only waits for units earlier in the
 // order, which were taken by running warps before it, so the scheme cannot
 // deadlock; a wait that exceeds ~20 s traps instead of hanging the GPU.
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -531,13 +532,16 @@ __global__ void __launch_bounds__(kConvThreads, 4) k_conv_flow(const FlowArgs a)
     const int p = static_cast<int>(u / a.batch);
     const int64_t pt = static_cast<int64_t>(u % a.batch);
     unsigned* fl = a.flags + pt * a.nunits;
+    // relaxed polling, then one acquire fence once the flag is seen set (an
+    // acquire load per poll would invalidate L1 every iteration)
     for (int e = a.dep_off[p] + lane; e < a.dep_off[p + 1]; e += 32) {
       const unsigned* f = fl + a.deps[e];
       long long spins = 0;
-      while (ld_acquire(f) == 0u) {
+      while (ld_relaxed(f) == 0u) {
         __nanosleep(32);
         if (++spins > (1ll << 28)) __trap();
       }
+      fence_acquire();
     }
     __syncwarp();
     band_task<M, CPLX, true>(a.arena, a.G, a.jobs, a.tasks + static_cast<int64_t>(p) * kSlots, a.W, pt, lane, sm, stg);
