@@ -261,6 +261,34 @@ def test_benchmark_configs_full_size_bitwise_vs_reference_engine(cfg, pid, m):
     assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"{cfg}: {pid} d=152 m={m} ({plan.conv_path(1)})")
 
 
+@pytest.mark.parametrize("pid,d,m", [("p1", 64, 4), ("p2", 40, 2), ("p1", 152, 10)])
+def test_complex_benchmark_graphs_bitwise_vs_reference_engine(pid, d, m):
+    """Complex mode (separate re/im slabs, the complex conv of pseries.cpp:49-59)
+    on the benchmark graphs, up to C2's full size, against the reference
+    engine."""
+    import os
+
+    if not po.has_ref():
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    p = po.gen_benchmark(pid, d, m, cplx=True, seed=7)
+    ref = po.evaluate(p, "ref", workers=os.cpu_count() or 1)
+    g = pe.build_jobgraph_shape(p.n, p.d, p.nvars, p.idx)
+    plan = pe.DevicePlan(g, m, "cplx", 0, 1)
+    vg, _, _ = plan.run(p.stat.reshape(p.P * m, *p.stat.shape[2:]), 1)
+    assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"complex {pid} d={d} m={m} ({plan.conv_path(1)})")
+
+
+@pytest.mark.parametrize("m", [2, 10])
+def test_exponents_at_full_degree_bitwise(m):
+    """Monomials with exponents (device fold_exponents prologue) at d=152."""
+    rng = np.random.default_rng(4242 + m)
+    for it in range(3):
+        p = md_instance(rng, m, False, nmax=6, Nmax=8, dmin=152, dmax=152, with_exponents=True)
+        ref = po.evaluate(p, "port")
+        vg, _ = dev_eval(p)
+        assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"exponents m={m} it={it}")
+
+
 def test_reference_binding_drop_in():
     """include/pse_b200_pseval.hpp compiled against the unmodified reference
     sources: run_device == run_sequential bit for bit on the reference's own
