@@ -202,6 +202,7 @@ struct BandSched {
 BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int W, int64_t cap_slots, bool flow, int64_t procs,
                         double slack, double ovh) {
   const int nb = 1 + d / W;  // band 0 = [0, d % W + 1), then full bands (kernels.cuh)
+  if (nb > 32767) throw std::invalid_argument("degree too large for the banded schedule");
   const int W0 = d % W + 1;
   auto lo = [&](int b) { return b == 0 ? 0 : W0 + (b - 1) * W; };
   const int nj = static_cast<int>(rows.size());
@@ -210,6 +211,7 @@ BandSched band_schedule(const std::vector<ConvRow>& rows, int d, int W, int64_t 
   std::vector<int64_t> base(nj + 1, 0);
   for (int j = 0; j < nj; ++j) base[j + 1] = base[j] + (rows[j].copy ? nb : nb * (nb + 1) / 2);
   const int64_t T = base[nj];
+  if (T >= (int64_t(1) << 31)) throw std::invalid_argument("graph too large for the banded schedule");
   auto fin = [&](int j, int b) { return rows[j].copy ? base[j] + b : base[j] + b * (b + 1) / 2 + b; };
   std::vector<int> tjob(T);
   std::vector<int16_t> tb(T), ts(T);  // ts = -1: copy task
