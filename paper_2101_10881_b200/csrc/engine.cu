@@ -501,7 +501,9 @@ struct Plan {
   // layers (e.g. C2's last layer) runs banded after the layered ones.
   int band_first(int batch) const {
     const int nl = static_cast<int>(layer_rows.size());
-    if (nrows_mine == 0 || conv_mode == 1) return nl;
+    const int64_t nb16 = 1 + d / 16;  // bands at the narrow width: the schedule's size bound
+    if (nrows_mine == 0 || conv_mode == 1 || nb16 > 32767 || nrows_mine * nb16 * (nb16 + 1) / 2 >= (int64_t(1) << 31))
+      return nl;
     if (conv_mode >= 2) return 0;
     const int64_t thr = int64_t(sms) * 4 * 128 * 2, npairs = (d + 2) / 2;
     if (static_cast<int64_t>(batch) * layer_pairs < thr) return 0;
