@@ -143,6 +143,11 @@ def cpu_sample(pid, d, m, threads: int, target_jobs: int):
     if po.has_ref():
         conv_ms, add_ms, wall_ms, J = po.ref_bench_sample(prob, threads, target_jobs)
         total = conv_ms * C / J + add_ms
+        if total < 2000.0:  # cheap enough (C1): the reference's own run_bench on the whole graph
+            _, _, wall, _ = po.ref_run_bench(prob, threads, 3)
+            return wall, "reference", threads, (f"reference run_bench (bench.cpp:17-50), run_parallel({threads} "
+                                                f"threads), whole graph: {C} conv + {g.add_job_count()} add jobs, "
+                                                f"median of 3")
         return total, "reference", threads, (f"reference run_parallel({threads} threads): first {J} of {C} conv "
                                              f"jobs of layer 1 timed and scaled x{C / J:.1f}, plus all {g.add_job_count()} add jobs")
     J = max(1, min(8, target_jobs))

@@ -443,6 +443,20 @@ def ref_parse_error(text: str) -> str:
 
 
 # ----------------------------------------------------------------- CPU timing
+def ref_run_bench(p: Problem, workers: int, repeats: int = 3):
+    """The reference's own run_bench (bench.cpp:17-50) on the whole graph:
+    returns (conv_ms, add_ms, wall_ms, gflops)."""
+    L = ref_lib()
+    h = _ref_handle(p)
+    try:
+        out = np.zeros(4, np.float64)
+        if L.ref_run_bench(h, workers, repeats, out) != 0:
+            raise _err(L, "ref")
+        return tuple(float(v) for v in out)
+    finally:
+        L.ref_problem_free(h)
+
+
 def ref_bench_sample(p: Problem, workers: int, njobs: int):
     """Reference run_parallel over the first njobs conv jobs of layer 1 plus all
     add layers; returns (conv_ms, add_ms, wall_ms, jobs_run)."""
