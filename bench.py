@@ -265,10 +265,11 @@ def ours(args, wl):
     if single_wave:
         upload(waves[0])
 
-    def step():
+    def step(detail=False):
         """one evaluation of every point this rank owns; device time from CUDA
-        events on the engine's stream around the whole step, the conv share
-        from the per-phase events of detail mode"""
+        events on the engine's stream around the whole step (the evaluation
+        is one CUDA-graph launch per wave); with detail, the phases run
+        un-captured with events between them, for the conv share"""
         conv = 0.0
         launches = 0
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -277,7 +278,7 @@ def ours(args, wl):
             if not single_wave:
                 upload(w)
                 launches += 1
-            r = plan.execute(len(w), detail=True)
+            r = plan.execute(len(w), detail=detail)
             stats["alg"] = r.alg_op_count
             conv += r.conv_ms
             launches += r.kernel_launches
@@ -287,6 +288,7 @@ def ours(args, wl):
 
     for _ in range(args.warmup):
         step()
+        step(detail=True)
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
@@ -306,6 +308,12 @@ def ours(args, wl):
     total_ms = D.max_over_ranks(my_total, red_dev)
     ms_per_step = total_ms / args.steps
     value = model_ops * total_points * args.steps / (total_ms * 1e-3) / 1e12
+    # conv share of the step (roofline): the same steps with per-phase events
+    convs = []
+    for _ in range(args.steps):
+        flush.random_(0, 255)
+        torch.cuda.synchronize(dev)
+        convs.append(step(detail=True)[1])
     conv_ms = sum(convs)
     path = plan.conv_path(wave)
     achieved = conv_ops * len(mine) * args.steps / (conv_ms * 1e-3)
