@@ -183,6 +183,17 @@ int pse_plan_exchange_words(const pse_plan* p, int32_t rank, int32_t batch, int6
 int pse_plan_pack(pse_plan* p, int32_t batch, double* dst);
 int pse_plan_unpack(pse_plan* p, int32_t batch, int32_t src_rank, const double* src);
 int pse_plan_finish(pse_plan* p, int32_t batch, int32_t detail, pse_report* rep);
+/* The same exchange without staging buffers or a collective: each rank maps
+ * the other ranks' arenas (CUDA IPC across processes -- NVLink peer memory on
+ * one node -- or a plan of the same process) and, once every rank's conv
+ * stage has finished (the caller's barrier), pse_plan_gather_peers copies the
+ * slots each peer produced straight from the peer's arena into its own (one
+ * kernel, peer loads). Then pse_plan_finish as above. */
+#define PSE_IPC_HANDLE_BYTES 64
+int pse_plan_arena_ipc_handle(const pse_plan* p, void* handle /* PSE_IPC_HANDLE_BYTES */);
+int pse_plan_open_peer(pse_plan* p, int32_t rank, const void* handle);
+int pse_plan_set_peer_arena(pse_plan* p, int32_t rank, const pse_plan* peer);
+int pse_plan_gather_peers(pse_plan* p, int32_t batch);
 
 /* plan geometry: out[8] = n, N, d, m, mode, total_slots, static_top, max_batch */
 int pse_plan_info(const pse_plan* p, int64_t* out);

@@ -105,6 +105,33 @@ __global__ void k_exchange(double* __restrict__ arena, double* __restrict__ buf,
   }
 }
 
+// Peer gather (one polynomial sharded over devices): every slot rank r
+// produced that the addition stage needs is copied from rank r's arena --
+// peer memory over NVLink (CUDA IPC mapping) or the same device -- into this
+// arena at the same offset (all ranks' arenas share the geometry). One launch
+// for all peers: item = (peer list entry, point, word).
+struct PeerList {
+  const double* src;  // peer arena
+  const int* slots;
+  int count;
+};
+__global__ void k_gather_peers(double* __restrict__ arena, Geom G, const PeerList* __restrict__ peers, int npeers,
+                               const int64_t* __restrict__ first, int batch) {
+  const int64_t n = first[npeers];
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int r = 0;
+    while (t >= first[r + 1]) ++r;
+    const int64_t u = t - first[r];
+    const int64_t w = u % G.slot_words;
+    const int64_t rest = u / G.slot_words;
+    const int i = static_cast<int>(rest % peers[r].count);
+    const int64_t b = rest / peers[r].count;
+    const int64_t off = b * G.point_words + static_cast<int64_t>(peers[r].slots[i]) * G.slot_words + w;
+    arena[off] = peers[r].src[off];
+  }
+}
+
 // arena -> reference DataArray layout [q][b][TS][d+1]
 __global__ void k_export(const double* __restrict__ arena, double* __restrict__ out, Geom G, int64_t TS, int batch) {
   const int d1 = G.d + 1;
@@ -449,6 +476,8 @@ struct Plan {
   // dynamic slots the addition stage needs from that rank (device lists)
   int rank = 0, nranks = 1;
   std::vector<std::pair<int*, int>> xslots;
+  std::vector<const double*> peer_arena;  // per rank (peer gather); opened IPC mappings are closed on destroy
+  std::vector<bool> peer_ipc;
   int2* ts = nullptr;
   int nts = 0;
   int* row_slot = nullptr;
@@ -594,6 +623,8 @@ struct Plan {
     cudaFree(vg);
     cudaFree(dyn);
     cudaFree(tri);
+    for (size_t r = 0; r < peer_arena.size(); ++r)
+      if (peer_ipc[r] && peer_arena[r]) cudaIpcCloseMemHandle(const_cast<double*>(peer_arena[r]));
     for (ConvGroup& gr : groups) {
       cudaFree(gr.prod);
       if (gr.join) cudaEventDestroy(gr.join);
@@ -1062,6 +1093,34 @@ void exchange(Plan& p, int batch, int rank, double* buf) {
   ck(cudaStreamSynchronize(p.stream), "exchange");
 }
 
+// copy every peer's addition-stage slots from its arena (peer_arena) into
+// ours; synchronous on the plan's stream
+void gather_peers(Plan& p, int batch) {
+  if (p.nranks < 2) throw std::invalid_argument("plan is not sharded");
+  if (batch < 1 || batch > p.max_batch) throw std::invalid_argument("batch outside [1, max_batch]");
+  ck(cudaSetDevice(p.device), "cudaSetDevice");
+  std::vector<PeerList> peers;
+  std::vector<int64_t> first(1, 0);
+  for (int r = 0; r < p.nranks; ++r) {
+    if (r == p.rank || p.xslots[r].second == 0) continue;
+    if (r >= static_cast<int>(p.peer_arena.size()) || !p.peer_arena[r])
+      throw std::invalid_argument("peer arena of rank " + std::to_string(r) + " not set");
+    peers.push_back({p.peer_arena[r], p.xslots[r].first, p.xslots[r].second});
+    first.push_back(first.back() + static_cast<int64_t>(batch) * p.xslots[r].second * p.G.slot_words);
+  }
+  if (peers.empty()) return;
+  PeerList* dpeers = dev_upload(peers, p.stream);
+  int64_t* dfirst = dev_upload(first, p.stream);
+  k_gather_peers<<<grid_for(first.back(), 256, p.sms), 256, 0, p.stream>>>(p.arena, p.G, dpeers,
+                                                                            static_cast<int>(peers.size()), dfirst, batch);
+  const cudaError_t e = cudaGetLastError();
+  const cudaError_t e2 = cudaStreamSynchronize(p.stream);
+  cudaFree(dpeers);
+  cudaFree(dfirst);
+  ck(e, "peer gather launch");
+  ck(e2, "peer gather");
+}
+
 // the addition stage of a sharded plan once every rank's slots are in place
 int finish(Plan& p, int batch, int detail, pse_report* rep) {
   if (p.nranks < 2) throw std::invalid_argument("plan is not sharded");
@@ -1264,6 +1323,68 @@ int pse_plan_unpack(pse_plan* p, int32_t batch, int32_t src_rank, const double* 
     if (!p) throw std::invalid_argument("null plan");
     if (src_rank == p->p->rank) return PSE_OK;  // own slots are already in place
     pse::exchange<false>(*p->p, batch, src_rank, const_cast<double*>(src));
+    return PSE_OK;
+  });
+}
+
+int pse_plan_arena_ipc_handle(const pse_plan* p, void* handle) {
+  return pse::guarded([&] {
+    if (!p || !handle) throw std::invalid_argument("null argument");
+    pse::ck(cudaSetDevice(p->p->device), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    pse::ck(cudaIpcGetMemHandle(&h, p->p->arena), "cudaIpcGetMemHandle");
+    static_assert(sizeof h == PSE_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof h);
+    return PSE_OK;
+  });
+}
+
+static void set_peer(pse::Plan& P, int rank, const double* ptr, bool ipc) {
+  if (P.nranks < 2) throw std::invalid_argument("plan is not sharded");
+  if (rank < 0 || rank >= P.nranks || rank == P.rank) throw std::invalid_argument("bad peer rank");
+  P.peer_arena.resize(P.nranks, nullptr);
+  P.peer_ipc.resize(P.nranks, false);
+  if (P.peer_ipc[rank] && P.peer_arena[rank]) cudaIpcCloseMemHandle(const_cast<double*>(P.peer_arena[rank]));
+  P.peer_arena[rank] = ptr;
+  P.peer_ipc[rank] = ipc;
+}
+
+int pse_plan_open_peer(pse_plan* p, int32_t rank, const void* handle) {
+  return pse::guarded([&] {
+    if (!p || !handle) throw std::invalid_argument("null argument");
+    pse::ck(cudaSetDevice(p->p->device), "cudaSetDevice");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    void* ptr = nullptr;
+    pse::ck(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    set_peer(*p->p, rank, static_cast<const double*>(ptr), true);
+    return PSE_OK;
+  });
+}
+
+int pse_plan_set_peer_arena(pse_plan* p, int32_t rank, const pse_plan* peer) {
+  return pse::guarded([&] {
+    if (!p || !peer) throw std::invalid_argument("null argument");
+    if (peer->p->TSdev != p->p->TSdev || peer->p->G.point_words != p->p->G.point_words)
+      throw std::invalid_argument("peer plan has a different arena geometry");
+    if (peer->p->device != p->p->device) {  // direct peer access between devices of this process
+      int ok = 0;
+      pse::ck(cudaDeviceCanAccessPeer(&ok, p->p->device, peer->p->device), "cudaDeviceCanAccessPeer");
+      if (!ok) throw std::invalid_argument("no peer access between the devices");
+      pse::ck(cudaSetDevice(p->p->device), "cudaSetDevice");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(peer->p->device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) pse::ck(e, "cudaDeviceEnablePeerAccess");
+      cudaGetLastError();
+    }
+    set_peer(*p->p, rank, peer->p->arena, false);
+    return PSE_OK;
+  });
+}
+
+int pse_plan_gather_peers(pse_plan* p, int32_t batch) {
+  return pse::guarded([&] {
+    if (!p) throw std::invalid_argument("null plan");
+    pse::gather_peers(*p->p, batch);
     return PSE_OK;
   });
 }

@@ -61,12 +61,44 @@ def sum_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
-def evaluate_sharded(plan, batch: int = 1, detail: bool = True):
+def connect_peers(plan) -> bool:
+    """Map every other rank's arena into this plan (CUDA IPC handles
+    exchanged over the process group once): NVLink peer memory between the
+    GPUs of a node, plain device memory when ranks share a GPU. Returns
+    False (and the collective exchange is used) when IPC is unavailable."""
+    import torch.distributed as dist
+
+    from ._lib import PseError
+
+    world = plan.nranks
+    try:
+        mine = plan.ipc_handle()
+    except PseError:
+        mine = b""
+    handles = [None] * world
+    dist.all_gather_object(handles, mine)
+    ok = all(h for h in handles)
+    if ok:
+        try:
+            for r, h in enumerate(handles):
+                if r != plan.rank:
+                    plan.open_peer(r, h)
+        except PseError:
+            ok = False
+    flags = [None] * world
+    dist.all_gather_object(flags, ok)
+    return all(flags)
+
+
+def evaluate_sharded(plan, batch: int = 1, detail: bool = True, p2p: bool = False):
     """One evaluation of a polynomial sharded over the process group: this
-    rank's conv share, all-gather of the addition-stage term blocks (a pure
-    copy of limbs -- NCCL over NVLink on GPUs, gloo through host memory when
-    testing several ranks on one device), then the exact addition tree on
-    every rank. Returns (conv_ms, exchange_ms, finish_ms)."""
+    rank's conv share, the exchange of the addition-stage term slots (a pure
+    copy of limbs), then the exact addition tree on every rank. The exchange
+    is either the peer gather (p2p, after connect_peers: every rank reads the
+    slots it lacks straight from the peers' arenas, between two barriers) or
+    an all-gather of packed blocks (NCCL over NVLink on GPUs, gloo through
+    host memory when several ranks share a device). Returns (conv_ms,
+    exchange_ms, finish_ms)."""
     import time
 
     import torch
@@ -74,9 +106,17 @@ def evaluate_sharded(plan, batch: int = 1, detail: bool = True):
 
     world = plan.nranks
     dev = torch.device(f"cuda:{plan.device}")
+    rep = plan.execute(batch, detail=detail)  # returns once the conv stage has finished
+    if p2p and world > 1:
+        t0 = time.perf_counter()
+        dist.barrier()  # every rank's term slots are final
+        plan.gather_peers(batch)
+        dist.barrier()  # every rank has read ours before our addition tree rewrites them
+        ex_ms = (time.perf_counter() - t0) * 1e3
+        fin = plan.finish(batch)
+        return rep.conv_ms, ex_ms, fin.wall_ms
     words = [plan.exchange_words(r, batch) for r in range(world)]
     width = max(1, max(words))
-    rep = plan.execute(batch, detail=detail)
     mine = torch.zeros(width, dtype=torch.float64, device=dev)
     t0 = time.perf_counter()
     plan.pack(mine.data_ptr(), batch)

@@ -414,6 +414,25 @@ class DevicePlan:
     def unpack(self, src_rank: int, src_ptr: int, batch: int = 1):
         check(lib().pse_plan_unpack(self._h, batch, src_rank, src_ptr))
 
+    def ipc_handle(self) -> bytes:
+        """CUDA IPC handle of this plan's arena (pse_plan_arena_ipc_handle)"""
+        buf = C.create_string_buffer(64)
+        check(lib().pse_plan_arena_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def open_peer(self, rank: int, handle: bytes):
+        """map rank's arena from its IPC handle (another process)"""
+        buf = C.create_string_buffer(bytes(handle), 64)
+        check(lib().pse_plan_open_peer(self._h, rank, buf))
+
+    def set_peer(self, rank: int, peer: "DevicePlan"):
+        """use another plan of this process as rank's arena"""
+        check(lib().pse_plan_set_peer_arena(self._h, rank, peer._h))
+
+    def gather_peers(self, batch: int = 1):
+        """copy the slots the peers produced from their arenas (after a barrier)"""
+        check(lib().pse_plan_gather_peers(self._h, batch))
+
     def finish(self, batch: int = 1, detail: bool = True) -> Report:
         rep = Report()
         check(lib().pse_plan_finish(self._h, batch, int(detail), C.byref(rep)))

@@ -338,6 +338,79 @@ def test_monomial_sharding_is_bit_exact(pid, d, m, nranks):
     assert_bitwise(ref_vg[:, 0].reshape(want.shape), want, "vs oracle")
 
 
+@pytest.mark.parametrize("pid,d,m,nranks", [("p1", 15, 2, 2), ("p3", 4, 2, 4), ("p2", 40, 3, 3)])
+def test_monomial_sharding_peer_gather_is_bit_exact(pid, d, m, nranks):
+    """The same sharding with the exchange done by pse_plan_gather_peers: each
+    rank copies the slots the other ranks produced straight out of their
+    arenas (here plans of one process on one device)."""
+    pr = pe.gen_benchmark(pid, d, m, seed=7)
+    g = pe.build_jobgraph_shape(pr.n, pr.d, pr.nvars, pr.indices)
+    full = pe.DevicePlan(g, m, "real", 0, 1)
+    ref_vg, _, _ = full.run(pr.stat, 1)
+    plans = [pe.DevicePlan(g, m, "real", 0, 1, rank=r, nranks=nranks) for r in range(nranks)]
+    for p in plans:
+        for q in plans:
+            if q is not p:
+                p.set_peer(q.rank, q)
+        p.upload(pr.stat, 1)
+        p.execute(1, detail=True)
+    for p in plans:
+        p.gather_peers(1)
+    for p in plans:
+        p.finish(1)
+        vg, _ = p.download(1)
+        assert_bitwise(vg, ref_vg, f"{pid} rank {p.rank}/{nranks} (peer gather)")
+
+
+def _ipc_worker(rank, world, port, outdir):
+    import os
+    import sys
+
+    import torch
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import paper_2101_10881_b200 as pe2
+    from paper_2101_10881_b200 import dist as DD
+
+    dist = DD.init("gloo")
+    torch.cuda.set_device(0)
+    pr = pe2.gen_benchmark("p1", 15, 2, seed=7)
+    g = pe2.build_jobgraph_shape(pr.n, pr.d, pr.nvars, pr.indices)
+    plan = pe2.DevicePlan(g, 2, "real", 0, 1, rank=rank, nranks=world)
+    assert DD.connect_peers(plan)
+    plan.upload(pr.stat, 1)
+    for _ in range(2):  # twice: the barriers also order consecutive evaluations
+        DD.evaluate_sharded(plan, 1, p2p=True)
+    vg, _ = plan.download(1)
+    np.save(os.path.join(outdir, f"vg{rank}.npy"), vg)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_monomial_sharding_ipc_processes_bit_exact(tmp_path):
+    """Two processes (ranks) sharing the GPU: arenas mapped through CUDA IPC
+    handles exchanged over gloo, the peer gather between barriers; both
+    ranks' results equal one device's bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_ipc_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    pr = pe.gen_benchmark("p1", 15, 2, seed=7)
+    g = pe.build_jobgraph_shape(pr.n, pr.d, pr.nvars, pr.indices)
+    ref_vg, _, _ = pe.DevicePlan(g, 2, "real", 0, 1).run(pr.stat, 1)
+    for r in range(2):
+        assert_bitwise(np.load(tmp_path / f"vg{r}.npy"), ref_vg, f"ipc rank {r}")
+
+
 def test_cli_verify_and_bench(tmp_path):
     """pseval_b200 verify / bench (the reference CLI's subcommands over the
     device engine); verify cross-checks the fused and split conv paths and
