@@ -88,3 +88,54 @@ def test_sharded_points_gloo_world2():
     assert got.shape == want.shape
     assert (got.view(np.uint64) == want.view(np.uint64)).all()  # bit-identical to one process
     assert slowest == 2.0 and count == total
+
+
+class _FakePlan:
+    """stands in for a sharded DevicePlan in connect_peers (host logic only)"""
+
+    def __init__(self, rank, world, fail_rank):
+        self.rank, self.nranks, self.fail_rank = rank, world, fail_rank
+        self.opened = {}
+
+    def ipc_handle(self):
+        from paper_2101_10881_b200._lib import PseError
+
+        if self.rank == self.fail_rank:
+            raise PseError(-2, "no IPC on this device")
+        return bytes([self.rank + 1]) * 64
+
+    def open_peer(self, r, h):
+        self.opened[r] = h
+
+
+def _peer_worker(rank, world, port, fail_rank, outdir):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    from paper_2101_10881_b200 import dist as DD
+
+    dist = DD.init("gloo")
+    plan = _FakePlan(rank, world, fail_rank)
+    ok = DD.connect_peers(plan)
+    np.save(os.path.join(outdir, f"r{rank}.npy"),
+            np.array([int(ok)] + [plan.opened.get(r, b"\0")[0] for r in range(world)]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_connect_peers_exchanges_handles_and_agrees_on_fallback(fail_rank):
+    """every rank maps every other rank's handle; if any rank cannot export
+    one, all ranks agree to fall back to the collective exchange"""
+    world = 3
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_peer_worker, args=(world, _free_port(), fail_rank, tmp), nprocs=world, join=True)
+        res = [np.load(os.path.join(tmp, f"r{r}.npy")) for r in range(world)]
+    for r, v in enumerate(res):
+        assert v[0] == (fail_rank < 0)
+        if fail_rank < 0:
+            assert [int(x) for x in v[1:]] == [0 if q == r else q + 1 for q in range(world)]
