@@ -560,7 +560,7 @@ struct Plan {
                               (produced.count(r.in1) ? 2 : 0) | (!r.copy && produced.count(r.in2) ? 4 : 0)));
       bw.jobs = dev_upload(v, stream);
     }
-    const int warps = sms * L->band_blocks_per_sm(flow()) * (kLaneThreads / 32);
+    const int warps = sms * L->band_blocks_per_sm(flow()) * (L->threads / 32);
     const int64_t cap_slots = std::max<int64_t>(kSlots, static_cast<int64_t>(kSlots * band_rounds * warps / batch));
     // per-task fixed cost in steps: ~4 us of hand-out / flags / partial sums
     // against one md_mul + md_add (instrumented ops; ~2000 ops per us-warp)

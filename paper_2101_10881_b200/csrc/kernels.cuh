@@ -148,11 +148,15 @@ struct Launchers {
   void (*md)(const MdArgs&, cudaStream_t);
   void (*prepare)();  // sets kernel attributes on the current device
   int lane_words;
+  int threads;        // threads per block of the lane kernels (per-M translation unit)
 };
 
 #ifdef PSE_KERNELS_IMPL
 
 constexpr int kConvThreads = kLaneThreads;
+// resident blocks per SM for a target expressed in 128-thread blocks (the
+// register budget stays the same whatever the block size)
+constexpr int blocks_for(int minb128) { return minb128 * 128 / kConvThreads > 0 ? minb128 * 128 / kConvThreads : 1; }
 constexpr int kAddThreads = kLaneThreads;
 
 // limb q of coefficient j at src[q*S + j]: one pointer walked by S (a 64-bit
@@ -210,7 +214,7 @@ constexpr int conv_default_minb() {
 }
 
 template <int M, bool CPLX, int MINB>
-__global__ void __launch_bounds__(kConvThreads, MINB) k_conv(const ConvArgs a) {
+__global__ void __launch_bounds__(kConvThreads, blocks_for(MINB)) k_conv(const ConvArgs a) {
   extern __shared__ double smem[];
   const Lane sm = make_lane(smem);
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -487,7 +491,7 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
 }
 
 template <int M, bool CPLX>
-__global__ void __launch_bounds__(kConvThreads, 4) k_conv_band(const BandArgs a) {
+__global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_band(const BandArgs a) {
   extern __shared__ double smem[];
   const Lane sm = make_lane(smem);
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -515,7 +519,7 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 }
 
 template <int M, bool CPLX>
-__global__ void __launch_bounds__(kConvThreads, 4) k_conv_flow(const FlowArgs a) {
+__global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_flow(const FlowArgs a) {
   extern __shared__ double smem[];
   const Lane sm = make_lane(smem);
   const int lane = threadIdx.x & 31;
@@ -907,7 +911,7 @@ struct Impl {
     cudaFuncSetAttribute(k_md<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
   }
   static const Launchers* table() {
-    static const Launchers L{&conv, &conv_band, &conv_flow, &band_blocks_per_sm, &conv_prod, &conv_accum, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE};
+    static const Launchers L{&conv, &conv_band, &conv_flow, &band_blocks_per_sm, &conv_prod, &conv_accum, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE, kLaneThreads};
     return &L;
   }
 };

@@ -1,5 +1,12 @@
 // Instantiation of the engine kernels for M = 4 limbs (real and complex).
 #define PSE_KERNELS_IMPL
+// 512-thread blocks (one per SM): the 16 warps an SM holds start together,
+// which keeps the instruction stream they share in cache (C2 -2%, C3' -6%
+// against four 128-thread blocks); the register and shared-memory budget per
+// thread is unchanged. M <= 2 keeps 128: its lighter threads fit more warps.
+#ifndef PSE_LANE_THREADS
+#define PSE_LANE_THREADS 512
+#endif
 #include "kernels.cuh"
 
 namespace pse {
