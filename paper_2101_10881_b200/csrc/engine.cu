@@ -510,10 +510,9 @@ struct Plan {
     std::vector<std::pair<int64_t, int>> waves;  // (first descriptor, descriptors)
     int* dep_off = nullptr;  // flow mode
     int* deps = nullptr;
+    unsigned* flags = nullptr;  // [batch][units]; per batch size, since a captured graph keeps its pointer
     int nunits = 0;
   };
-  unsigned* flow_flags = nullptr;  // [max_batch][units] (grown on demand)
-  int64_t flow_flag_words = 0;
   unsigned long long* flow_counter = nullptr;
   std::map<int, BandWaves> band_waves;
   int conv_mode = 0;         // PSE_CONV_MODE: 0 auto, 1 layered, 2 banded waves, 3 dataflow
@@ -593,12 +592,7 @@ struct Plan {
     if (flow()) {
       bw.dep_off = dev_upload(sch.dep_off, stream);
       bw.deps = dev_upload(sch.deps, stream);
-      const int64_t need = static_cast<int64_t>(batch) * bw.nunits;
-      if (need > flow_flag_words) {
-        cudaFree(flow_flags);
-        flow_flags = dev_alloc<unsigned>(static_cast<size_t>(need));
-        flow_flag_words = need;
-      }
+      bw.flags = dev_alloc<unsigned>(static_cast<size_t>(batch) * bw.nunits);
       if (!flow_counter) flow_counter = dev_alloc<unsigned long long>(1);
     }
     ck(cudaStreamSynchronize(stream), "band upload");
@@ -613,8 +607,8 @@ struct Plan {
       cudaFree(w.jobs);
       cudaFree(w.dep_off);
       cudaFree(w.deps);
+      cudaFree(w.flags);
     }
-    cudaFree(flow_flags);
     cudaFree(flow_counter);
     for (cudaEvent_t x : ev) cudaEventDestroy(x);
     for (void* p : owned) cudaFree(p);
@@ -691,9 +685,9 @@ struct Plan {
     if (first < static_cast<int>(layer_rows.size())) {  // banded part
       const BandWaves& bw = band_waves.at(batch);
       if (flow()) {
-        ck(cudaMemsetAsync(flow_flags, 0, sizeof(unsigned) * batch * bw.nunits, stream), "flags");
+        ck(cudaMemsetAsync(bw.flags, 0, sizeof(unsigned) * batch * bw.nunits, stream), "flags");
         ck(cudaMemsetAsync(flow_counter, 0, sizeof(unsigned long long), stream), "counter");
-        FlowArgs a{arena, G, bw.jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, flow_flags, flow_counter, bw.W};
+        FlowArgs a{arena, G, bw.jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, bw.flags, flow_counter, bw.W};
         L->conv_flow(a, sms * L->band_blocks_per_sm(true), stream);
         ++launches;
       } else {

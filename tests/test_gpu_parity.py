@@ -411,6 +411,31 @@ def test_monomial_sharding_ipc_processes_bit_exact(tmp_path):
         assert_bitwise(np.load(tmp_path / f"vg{r}.npy"), ref_vg, f"ipc rank {r}")
 
 
+def test_plan_reused_across_batch_sizes():
+    """One plan run at batch 1, 3 and 1 again through its captured CUDA
+    graphs (the dataflow path keeps per-batch task tables and flags): every
+    run equals the single-point evaluation bit for bit."""
+    base = po.gen_benchmark("p2", 40, 2, seed=7)
+    Q = base.P * base.m
+    top = base.stat.shape[2]
+    stat = np.empty((Q, 3, top, 41))
+    refs = []
+    for b in range(3):
+        zb = po.gen_benchmark("p2", 40, 2, seed=1000 + b)
+        st = base.stat.copy()
+        st[:, :, 1 + base.N:] = zb.stat[:, :, 1 + base.N:]
+        stat[:, b] = st.reshape(Q, top, 41)
+        refs.append(po.evaluate(po.Problem(base.n, base.d, base.m, False, base.nvars, base.idx, None, st), "port"))
+    g = pe.build_jobgraph_shape(base.n, base.d, base.nvars, base.idx)
+    plan = pe.DevicePlan(g, 2, "real", 0, 3)
+    for batch in (1, 3, 1, 3):
+        plan.upload(np.ascontiguousarray(stat[:, :batch]), batch)
+        plan.execute(batch, detail=False)
+        vg, _ = plan.download(batch)
+        for b in range(batch):
+            assert_bitwise(vg[:, b].reshape(refs[b].shape), refs[b], f"batch {batch} point {b} ({plan.conv_path(batch)})")
+
+
 def test_cli_verify_and_bench(tmp_path):
     """pseval_b200 verify / bench (the reference CLI's subcommands over the
     device engine); verify cross-checks the fused and split conv paths and
