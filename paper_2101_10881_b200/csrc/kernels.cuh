@@ -208,6 +208,14 @@ __device__ __forceinline__ void copy_md(double (&d)[M], const double (&s)[M]) {
 // registers, 3 -> 168, 2 -> 255). Large M trade occupancy for the ILP that
 // ptxas only exposes with more registers; selectable at run time for tuning
 // (PSE_CONV_MINB), default from conv_default_minb<M>().
+// complex convolutions keep the real accumulator in the lane (55 rows at
+// M = 10) for M >= 5; small M keep both in registers so that the dataflow
+// kernel's operand staging still fits next to the lanes
+template <int M>
+__host__ __device__ constexpr bool cplx_acc_lane() {
+  return M >= 5;
+}
+
 template <int M>
 constexpr int conv_default_minb() {
   return 4;
@@ -266,35 +274,52 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(MINB)) k_conv(const C
       if (i == kk) store_md<M>(Z, S, kk, o);
     }
   } else {
-    double ar[M], ai[M];  // accumulators (re, im)
+    // accumulators (re, im). For M >= 5 the real one lives in the lane
+    // (cplx_acc_lane), so its M registers are free while the four md_muls
+    // run; the real part is added as soon as it is formed. The reference's
+    // order per product (pseries.cpp:49-59) is kept: re = mul(xr,yr) -
+    // mul(xi,yi); im = mul(xr,yi) + mul(xi,yr); acc += each -- the two
+    // accumulations are independent, so doing re's first changes nothing.
+    constexpr bool LANE_RE = cplx_acc_lane<M>();
+    double ar[LANE_RE ? 1 : M], ai[M], o[M];
+    if constexpr (LANE_RE) acc_init<M>(sm);
 #pragma unroll 1
     for (int t = 0; t < total; ++t) {
       const bool second = t >= n1;
       const int kk = second ? k2 : k1;
       const int i = second ? t - n1 : t;
-      // (xr + i xi)(yr + i yi): pseries.cpp:50-51 operand order
-      double xr[M], yr[M], xi[M], yi[M], p1[M], p2[M], pre[M], pim[M];
-      load_md<M>(X, S, i, xr);
-      load_md<M>(Y, S, kk - i, yr);
-      load_md<M>(X + M * S, S, i, xi);
-      load_md<M>(Y + M * S, S, kk - i, yi);
-      exp_mul_fast<M>(xr, yr, p1, sm);
-      exp_mul_fast<M>(xi, yi, p2, sm);
-      exp_sub_fast<M>(p1, p2, pre, sm);
-      exp_mul_fast<M>(xr, yi, p1, sm);
-      exp_mul_fast<M>(xi, yr, p2, sm);
-      exp_add_fast<M>(p1, p2, pim, sm);
-      if (i == 0) {
-        copy_md<M>(ar, pre);
-        copy_md<M>(ai, pim);
+      // (xr + i xi)(yr + i yi): pseries.cpp:50-51 operand order; each md_mul
+      // loads its own operands (L1 hits) so that at most one pair is live
+      double xa[M], yb[M], p1[M], p2[M], pr[M];
+      load_md<M>(X, S, i, xa);
+      load_md<M>(Y, S, kk - i, yb);
+      exp_mul_fast<M>(xa, yb, p1, sm);  // xr * yr
+      load_md<M>(X + M * S, S, i, xa);
+      load_md<M>(Y + M * S, S, kk - i, yb);
+      exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yi
+      exp_sub_fast<M>(p1, p2, pr, sm);
+      if constexpr (LANE_RE) {
+        if (i == 0) {
+          copy_md<M>(o, pr);
+          acc_store<M>(pr, sm);
+        } else {
+          acc_add<M>(pr, o, sm);
+        }
+        if (i == kk) store_md<M>(Z, S, kk, o);
       } else {
-        exp_add_fast<M>(ar, pre, ar, sm);
-        exp_add_fast<M>(ai, pim, ai, sm);
+        if (i == 0) copy_md<M>(ar, pr);
+        else exp_add_fast<M>(ar, pr, ar, sm);
+        if (i == kk) store_md<M>(Z, S, kk, ar);
       }
-      if (i == kk) {
-        store_md<M>(Z, S, kk, ar);
-        store_md<M>(Z + M * S, S, kk, ai);
-      }
+      load_md<M>(X, S, i, xa);
+      exp_mul_fast<M>(xa, yb, p1, sm);  // xr * yi
+      load_md<M>(X + M * S, S, i, xa);
+      load_md<M>(Y, S, kk - i, yb);
+      exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yr
+      exp_add_fast<M>(p1, p2, pr, sm);
+      if (i == 0) copy_md<M>(ai, pr);
+      else exp_add_fast<M>(ai, pr, ai, sm);
+      if (i == kk) store_md<M>(Z + M * S, S, kk, ai);
     }
   }
 }
@@ -450,42 +475,66 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
       if (i == (second ? ibB : ibA)) store_md<M>(Z, S, k, o);
     }
   } else {
-    double ar[M], ai[M];
+    // as k_conv's complex branch (real accumulator in the lane for M >= 5)
+    constexpr bool LANE_RE = cplx_acc_lane<M>();
+    double ar[LANE_RE ? 1 : M], ai[M], o[M];
+    if constexpr (LANE_RE) acc_init<M>(sm);
 #pragma unroll 1
     for (int t = 0; t < total; ++t) {
       const bool second = t >= nA;
       const int k = second ? kB : kA;
       const int ia = second ? iaB : iaA;
       const int i = second ? iaB + (t - nA) : iaA + t;
-      double xr[M], yr[M], xi[M], yi[M], p1[M], p2[M], pre[M], pim[M];
-      ldx(0, i, xr);
-      ldy(0, k - i, yr);
-      ldx(1, i, xi);
-      ldy(1, k - i, yi);
-      exp_mul_fast<M>(xr, yr, p1, sm);
-      exp_mul_fast<M>(xi, yi, p2, sm);
-      exp_sub_fast<M>(p1, p2, pre, sm);
-      exp_mul_fast<M>(xr, yi, p1, sm);
-      exp_mul_fast<M>(xi, yr, p2, sm);
-      exp_add_fast<M>(p1, p2, pim, sm);
+      const bool last = i == (second ? ibB : ibA);
+      double xa[M], yb[M], p1[M], p2[M], pr[M];  // one operand pair live at a time
+      ldx(0, i, xa);
+      ldy(0, k - i, yb);
+      exp_mul_fast<M>(xa, yb, p1, sm);  // xr * yr
+      ldx(1, i, xa);
+      ldy(1, k - i, yb);
+      exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yi
+      exp_sub_fast<M>(p1, p2, pr, sm);
+      if constexpr (LANE_RE) {
+        if (i == 0) {
+          copy_md<M>(o, pr);
+          acc_store<M>(pr, sm);
+        } else {
+          if (i == ia) {  // resume the partial sums of the previous segment
+#pragma unroll
+            for (int q = 0; q < M; ++q) o[q] = __ldcg(Z + q * S + k);
+            acc_store<M>(o, sm);
+          }
+          acc_add<M>(pr, o, sm);
+        }
+        if (last) store_md<M>(Z, S, k, o);
+      } else {
+        if (i == 0) {
+          copy_md<M>(ar, pr);
+        } else {
+          if (i == ia) {
+#pragma unroll
+            for (int q = 0; q < M; ++q) ar[q] = __ldcg(Z + q * S + k);
+          }
+          exp_add_fast<M>(ar, pr, ar, sm);
+        }
+        if (last) store_md<M>(Z, S, k, ar);
+      }
+      ldx(0, i, xa);
+      exp_mul_fast<M>(xa, yb, p1, sm);  // xr * yi
+      ldx(1, i, xa);
+      ldy(0, k - i, yb);
+      exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yr
+      exp_add_fast<M>(p1, p2, pr, sm);
       if (i == 0) {
-        copy_md<M>(ar, pre);
-        copy_md<M>(ai, pim);
+        copy_md<M>(ai, pr);
       } else {
         if (i == ia) {
 #pragma unroll
-          for (int q = 0; q < M; ++q) {
-            ar[q] = __ldcg(Z + q * S + k);
-            ai[q] = __ldcg(Z + (M + q) * S + k);
-          }
+          for (int q = 0; q < M; ++q) ai[q] = __ldcg(Z + (M + q) * S + k);
         }
-        exp_add_fast<M>(ar, pre, ar, sm);
-        exp_add_fast<M>(ai, pim, ai, sm);
+        exp_add_fast<M>(ai, pr, ai, sm);
       }
-      if (i == (second ? ibB : ibA)) {
-        store_md<M>(Z, S, k, ar);
-        store_md<M>(Z + M * S, S, k, ai);
-      }
+      if (last) store_md<M>(Z + M * S, S, k, ai);
     }
   }
 }
@@ -526,7 +575,7 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_flow(const
   const int64_t units = static_cast<int64_t>(a.nunits) * a.batch;
   // per-warp staging area after the lanes (band_stage)
   constexpr int Q = CPLX ? 2 * M : M;
-  double* stg = smem + kLaneThreads * (CPLX ? MdTraits<M>::LANE : MdTraits<M>::LANE_CONV) +
+  double* stg = smem + kLaneThreads * (CPLX && !cplx_acc_lane<M>() ? MdTraits<M>::LANE : MdTraits<M>::LANE_CONV) +
                 (threadIdx.x >> 5) * kStageSlots * Q;
   for (;;) {
     unsigned long long u = 0;
@@ -811,7 +860,8 @@ template <int M, bool CPLX>
 struct Impl {
   static size_t smem(int threads) { return static_cast<size_t>(threads) * MdTraits<M>::LANE * sizeof(double); }
   static size_t smem_conv(int threads) {
-    return static_cast<size_t>(threads) * (CPLX ? MdTraits<M>::LANE : MdTraits<M>::LANE_CONV) * sizeof(double);
+    return static_cast<size_t>(threads) * (CPLX && !cplx_acc_lane<M>() ? MdTraits<M>::LANE : MdTraits<M>::LANE_CONV) *
+           sizeof(double);
   }
   static int minb() {
     static const int v = [] {
