@@ -556,7 +556,8 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_band(const
 // (relaxed polls of their flags + an acquire fence), run the task and publish their own flag
 // (stores, fence, release). A unit only waits for units earlier in the
 // order, which were taken by running warps before it, so the scheme cannot
-// deadlock; a wait that exceeds ~20 s traps instead of hanging the GPU.
+// deadlock; a wait that exceeds ~10 s (global timer) traps instead of
+// hanging the GPU.
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -589,10 +590,16 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_flow(const
     // acquire load per poll would invalidate L1 every iteration)
     for (int e = a.dep_off[p] + lane; e < a.dep_off[p + 1]; e += 32) {
       const unsigned* f = fl + a.deps[e];
-      long long spins = 0;
+      unsigned spins = 0;
+      unsigned long long t0 = 0;
       while (ld_relaxed(f) == 0u) {
         __nanosleep(32);
-        if (++spins > (1ll << 28)) __trap();
+        if ((++spins & 1023u) == 0u) {  // a dependency that never completes: trap after ~10 s
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > 10000000000ull) __trap();
+        }
       }
       fence_acquire();
     }
