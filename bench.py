@@ -486,10 +486,17 @@ def main():
     args = ap.parse_args()
     if args.m:
         pid, d, m, ppg, desc = WORKLOADS[args.workload]
-        names = {1: "double", 2: "double-double", 3: "triple double", 4: "quad double", 5: "penta double",
-                 8: "octo double", 10: "deca double"}
-        WORKLOADS[args.workload] = (pid, d, args.m, ppg, desc.replace("deca double", names[args.m]).replace(
-            "d=152", f"d=152, m={args.m}") if args.m != m else desc)
+        if args.m != m:
+            names = {1: "double", 2: "double-double", 3: "triple double", 4: "quad double", 5: "penta double",
+                     8: "octo double", 10: "deca double"}
+            for old in sorted(names.values(), key=len, reverse=True):  # "double-double" before "double"
+                if desc.endswith(", " + old):
+                    desc = desc[: -len(old)] + names[args.m]
+                    break
+            else:
+                desc += ", " + names[args.m]
+            desc += f" (m={args.m})"
+        WORKLOADS[args.workload] = (pid, d, args.m, ppg, desc)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

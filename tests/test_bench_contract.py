@@ -45,3 +45,16 @@ def test_reference_arm_other_ranks_exit_quietly():
     """under torchrun only rank 0 runs and prints the reference arm"""
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
     assert run_bench("--impl", "reference", "--workload", "c1", "--steps", "1", env=env).strip() == ""
+
+
+def test_reference_arm_precision_override():
+    """--m runs the C3 sweep points (here the reference arm on C1's graph at m=1)"""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    if not po.has_ref():
+        pytest.skip("oracle/_ref not built")
+    d = json.loads(run_bench("--impl", "reference", "--workload", "c1", "--m", "1", "--steps", "1",
+                             "--warmup", "3").strip())
+    assert d["config"]["workload"].endswith("d=15, double (m=1)")
+    assert d["value"] > 0
