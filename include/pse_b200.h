@@ -87,8 +87,12 @@ typedef struct {
   const int64_t *ts_slot, *ts_factor;
 } pse_graph_desc;
 
-/* RunReport (executor.hpp:31-43) plus device timings. All times are CUDA-event
- * milliseconds on the plan's stream. */
+/* RunReport (executor.hpp:31-43) plus device timings, in milliseconds.
+ * wall/conv/scale/add come from the kernels' own %globaltimer stamps of the
+ * run (a phase ends when all of its jobs and those of the earlier phases are
+ * done; executor.cpp:154-157 records the same per-phase split); per-layer
+ * times: pse_plan_layer_ms. The other times are CUDA events on the plan's
+ * stream. */
 typedef struct {
   double wall_ms;  /* conv + scale + add phases (the paper's "wall") */
   double conv_ms, scale_ms, add_ms;
@@ -98,6 +102,8 @@ typedef struct {
   int64_t conv_jobs_executed, add_jobs_executed, copy_jobs_executed; /* all points */
   int32_t batch;
   int32_t kernel_launches; /* device kernels launched by the call */
+  double device_ms;        /* events around the whole device evaluation (CUDA-graph replay) */
+  double exchange_ms;      /* sharded plans (pse_plan_finish): conv end -> addition-stage start */
 } pse_report;
 
 const char* pse_last_error(void);
@@ -165,6 +171,10 @@ int pse_plan_download(pse_plan* p, int32_t batch, double* const* value_grad_out,
  * contract over a DataArray (batch = 1) or a batch of points */
 int pse_plan_run(pse_plan* p, int32_t batch, const double* const* static_slabs, int64_t point_stride,
                  double* const* dyn_slabs_out, double* const* value_grad_out, pse_report* rep);
+/* per-layer phase times of the plan's last run (RunReport::conv_layer_ms /
+ * add_layer_ms, executor.hpp:31-43, filled per phase at executor.cpp:154-157):
+ * n_conv / n_add must equal the graph's conv / add layer counts */
+int pse_plan_layer_ms(const pse_plan* p, double* conv_layer_ms, int32_t n_conv, double* add_layer_ms, int32_t n_add);
 /* ---- one polynomial sharded over devices (one plan per GPU) --------------
  * Rank r's plan executes only the convolution jobs of its share of the
  * independent job groups (whole monomials, contiguous and balanced by job

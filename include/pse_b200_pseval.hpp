@@ -15,13 +15,16 @@
 // std::runtime_error otherwise.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "pse_b200.h"
-#include "pseval/executor.hpp"  // the reference's own header (proj/include)
+#include "pseval/bench.hpp"     // the reference's own headers (proj/include)
+#include "pseval/executor.hpp"
+#include "pseval/gen.hpp"
 
 namespace pseval {
 
@@ -124,10 +127,16 @@ inline RunReport run_device(const JobGraph& g, DataArray& a, const DeviceOptions
     out[q] = vg.data() + static_cast<size_t>(q) * rows * (a.d + 1);
   }
   pse_report rep{};
-  const int rc = pse_plan_run(plan, 1, in.data(), a.total_slots * (a.d + 1), dyn.data(), out.data(), &rep);
+  RunReport r;
+  // per-phase times (executor.cpp:154-157): one entry per conv / add layer
+  r.conv_layer_ms.assign(g.conv_layers.size(), 0.0);
+  r.add_layer_ms.assign(g.add_layers.size(), 0.0);
+  int rc = pse_plan_run(plan, 1, in.data(), a.total_slots * (a.d + 1), dyn.data(), out.data(), &rep);
+  if (rc == PSE_OK)
+    rc = pse_plan_layer_ms(plan, r.conv_layer_ms.data(), static_cast<int32_t>(r.conv_layer_ms.size()),
+                           r.add_layer_ms.data(), static_cast<int32_t>(r.add_layer_ms.size()));
   pse_plan_destroy(plan);
   b200_detail::check(rc);
-  RunReport r;
   r.value = b200_detail::read_row(vg, rows, 0, a.d, a.m, a.mode);
   for (int i = 0; i < g.n; ++i) r.gradient.push_back(b200_detail::read_row(vg, rows, 1 + i, a.d, a.m, a.mode));
   r.wall_ms = rep.wall_ms;
@@ -135,6 +144,40 @@ inline RunReport run_device(const JobGraph& g, DataArray& a, const DeviceOptions
   r.conv_jobs_executed = static_cast<long>(rep.conv_jobs_executed);
   r.add_jobs_executed = static_cast<long>(rep.add_jobs_executed);
   return r;
+}
+
+// run_bench (bench.cpp:17-50) with run_device in place of run_parallel /
+// run_sequential -- the one-line engine switch INTEGRATION.md describes: same
+// graph, fold, stage, median-of-repeats record, conv_ms / add_ms from the
+// RunReport's per-layer lists
+inline BenchRecord run_bench_device(const Problem& p, int repeats, const DeviceOptions& opt = {}) {
+  if (repeats < 1) repeats = 1;
+  const JobGraph g = build_jobgraph(p.poly);
+  const Polynomial folded = fold_polynomial(p.poly, p.z);
+  std::vector<RunReport> runs;
+  for (int r = 0; r < repeats; ++r) {
+    DataArray a = stage(folded, p.z);
+    runs.push_back(run_device(g, a, opt));
+  }
+  std::vector<size_t> order(runs.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](size_t x, size_t y) { return runs[x].wall_ms < runs[y].wall_ms; });
+  const RunReport& mid = runs[order[(order.size() - 1) / 2]];
+  BenchRecord rec;
+  rec.id = p.id;
+  rec.d = p.poly.d;
+  rec.m = p.poly.a0.m;
+  rec.mode = p.poly.a0.mode;
+  rec.workers = 0;
+  rec.conv_jobs = g.conv_job_count();
+  rec.add_jobs = g.add_job_count();
+  rec.conv_ms = mid.conv_ms();
+  rec.add_ms = mid.add_ms();
+  rec.sum_ms = rec.conv_ms + rec.add_ms;
+  rec.wall_ms = mid.wall_ms;
+  rec.double_ops = mid.double_op_count;
+  rec.gflops = mid.wall_ms > 0 ? static_cast<double>(mid.double_op_count) / (mid.wall_ms * 1e6) : 0.0;
+  return rec;
 }
 
 // evaluate (executor.cpp:271-276) with the device engine

@@ -4,6 +4,7 @@
 // bit on the reference's DataArray (value, every gradient, the whole arena).
 // Built by oracle/Makefile into oracle/_ref/integration_check (needs the
 // reference sources); run by tests/test_gpu_parity.py on a GPU box.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -41,6 +42,29 @@ int main(int argc, char** argv) {
     ++runs;
   }
   std::printf("%s: %d/%d configurations bitwise identical\n", bad ? "FAIL" : "OK", runs - bad, runs);
+
+  // RunReport timings through the drop-in: the reference's run_bench
+  // (bench.cpp:17-50) with run_device as its engine. conv_ms()/add_ms() sum
+  // the per-layer lists (executor.cpp:154-157, one entry per layer) and,
+  // with the (empty) scale phase, account for wall_ms.
+  int tbad = 0;
+  for (const Cfg& c : {Cfg{"p1", 15, 2, Mode::real}, Cfg{"p3", 40, 4, Mode::real}}) {
+    const Problem p = gen_benchmark(c.id, c.d, c.m, c.mode, 7);
+    const JobGraph g = build_jobgraph(p.poly);
+    DataArray a = stage(p.poly, p.z);
+    const RunReport r = run_device(g, a);
+    const BenchRecord b = run_bench_device(p, 3);
+    const bool lists = r.conv_layer_ms.size() == g.conv_layers.size() && r.add_layer_ms.size() == g.add_layers.size();
+    const bool pos = b.conv_ms > 0 && b.add_ms > 0 && b.wall_ms > 0;
+    const double gap = std::fabs(b.conv_ms + b.add_ms - b.wall_ms) / b.wall_ms;
+    const bool ok = lists && pos && gap <= 0.01;
+    std::printf("run_bench via run_device %s d=%d m=%d: conv %.4f ms + add %.4f ms vs wall %.4f ms (%zu + %zu layers) %s\n",
+                c.id, c.d, c.m, b.conv_ms, b.add_ms, b.wall_ms, r.conv_layer_ms.size(), r.add_layer_ms.size(),
+                ok ? "ok" : "BAD");
+    tbad += ok ? 0 : 1;
+  }
+  std::printf("%s: RunReport per-layer timings\n", tbad ? "FAIL" : "OK");
+  bad += tbad;
   (void)argc;
   (void)argv;
   return bad;

@@ -50,6 +50,7 @@ class Report(C.Structure):
         ("double_op_count", C.c_int64), ("alg_op_count", C.c_int64),
         ("conv_jobs_executed", C.c_int64), ("add_jobs_executed", C.c_int64), ("copy_jobs_executed", C.c_int64),
         ("batch", C.c_int32), ("kernel_launches", C.c_int32),
+        ("device_ms", C.c_double), ("exchange_ms", C.c_double),
     ]
 
 
@@ -64,6 +65,7 @@ EXPORTS = [
     "pse_problem_parse", "pse_problem_read", "pse_problem_write", "pse_problem_text", "pse_problem_create",
     "pse_problem_gen", "pse_problem_info", "pse_problem_id", "pse_problem_arrays", "pse_problem_destroy",
     "pse_plan_create_sharded", "pse_plan_exchange_words", "pse_plan_pack", "pse_plan_unpack", "pse_plan_finish",
+    "pse_plan_layer_ms",
 ]
 
 _lib = None
@@ -130,6 +132,7 @@ def lib():
     L.pse_plan_pack.argtypes = [_VP, i32, dp]
     L.pse_plan_unpack.argtypes = [_VP, i32, i32, dp]
     L.pse_plan_finish.argtypes = [_VP, i32, i32, C.POINTER(Report)]
+    L.pse_plan_layer_ms.argtypes = [_VP, dp, i32, dp, i32]
     _lib = L
     return L
 

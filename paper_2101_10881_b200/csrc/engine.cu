@@ -116,13 +116,14 @@ struct PeerList {
   int count;
 };
 __global__ void k_gather_peers(double* __restrict__ arena, Geom G, const PeerList* __restrict__ peers, int npeers,
-                               const int64_t* __restrict__ first, int batch) {
-  const int64_t n = first[npeers];
+                               const int64_t* __restrict__ first1, int batch) {
+  // first1[r]: words before peer entry r for ONE point; a batch scales it
+  const int64_t n = first1[npeers] * batch;
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int r = 0;
-    while (t >= first[r + 1]) ++r;
-    const int64_t u = t - first[r];
+    while (t >= first1[r + 1] * batch) ++r;
+    const int64_t u = t - first1[r] * batch;
     const int64_t w = u % G.slot_words;
     const int64_t rest = u / G.slot_words;
     const int i = static_cast<int>(rest % peers[r].count);
@@ -471,13 +472,24 @@ struct Plan {
   std::vector<std::pair<int4*, int>> pro_layers;
   std::vector<ConvGroup> groups;
   cudaEvent_t fork = nullptr;
-  std::vector<std::pair<int2*, int>> add_layers;
+  std::vector<std::pair<int2*, int>> add_layers;  // non-empty graph add layers
+  std::vector<int> add_layer_index;                // their graph add layer
+  int n_conv_layers = 0, n_add_layers = 0;         // graph layers (RunReport entries)
+  Stamp* stamps = nullptr;                         // phase stamps of the last run (device)
+  std::vector<double> conv_layer_ms, add_layer_ms; // per-layer times of the last run
+  double exchange_ms = 0;                          // sharded: conv end -> tail start
   // sharding one polynomial over devices: this plan's rank, and per rank the
   // dynamic slots the addition stage needs from that rank (device lists)
   int rank = 0, nranks = 1;
   std::vector<std::pair<int*, int>> xslots;
   std::vector<const double*> peer_arena;  // per rank (peer gather); opened IPC mappings are closed on destroy
   std::vector<bool> peer_ipc;
+  // device copy of the peer list for the gather kernel, rebuilt when a peer changes
+  PeerList* peer_list = nullptr;
+  int64_t* peer_first = nullptr;
+  int npeer_list = 0;
+  int64_t peer_words1 = 0;  // words gathered per point
+  bool peers_dirty = true;
   int2* ts = nullptr;
   int nts = 0;
   int* row_slot = nullptr;
@@ -521,6 +533,10 @@ struct Plan {
   int band_w = 0;            // PSE_BAND_W: 16 or 32 (0: chosen per run)
   double flow_procs = 1.0;   // PSE_FLOW_PROCS: simulated warps, as a fraction of the resident ones
   int64_t layer_pairs = 0;   // average conv layer size in coefficient pairs
+  // some dynamic slot is written by more than one conv job (validate(), like
+  // the reference, accepts a slot rewritten in a later layer): the banded
+  // schedule assumes one producer per slot, so such graphs stay layered
+  bool multi_writer = false;
 
   // First conv layer the banded path runs for this batch (layer_rows.size():
   // none). A layer is "small" when it offers less than two waves of resident
@@ -530,7 +546,8 @@ struct Plan {
   int band_first(int batch) const {
     const int nl = static_cast<int>(layer_rows.size());
     const int64_t nb16 = 1 + d / 16;  // bands at the narrow width: the schedule's size bound
-    if (nrows_mine == 0 || conv_mode == 1 || nb16 > 32767 || nrows_mine * nb16 * (nb16 + 1) / 2 >= (int64_t(1) << 31))
+    if (nrows_mine == 0 || conv_mode == 1 || multi_writer || nb16 > 32767 ||
+        nrows_mine * nb16 * (nb16 + 1) / 2 >= (int64_t(1) << 31))
       return nl;
     if (conv_mode >= 2) return 0;
     const int64_t thr = int64_t(sms) * 4 * 128 * 2, npairs = (d + 2) / 2;
@@ -549,14 +566,22 @@ struct Plan {
     BandWaves bw;
     bw.first = band_first(batch);
     std::vector<ConvRow> rows;
-    for (size_t L2 = bw.first; L2 < layer_rows.size(); ++L2) rows.insert(rows.end(), layer_rows[L2].begin(), layer_rows[L2].end());
-    {  // job table; flag bits 2/4: in1/in2 produced inside the banded part
+    std::vector<int> row_layer;
+    for (size_t L2 = bw.first; L2 < layer_rows.size(); ++L2) {
+      rows.insert(rows.end(), layer_rows[L2].begin(), layer_rows[L2].end());
+      row_layer.insert(row_layer.end(), layer_rows[L2].size(), static_cast<int>(L2));
+    }
+    {  // job table; flag bits 2/4: in1/in2 produced inside the banded part;
+       // bits 8+: the graph conv layer (phase stamps)
       std::set<int64_t> produced;
       for (auto& r : rows) produced.insert(r.out);
       std::vector<int4> v;
-      for (auto& r : rows)
+      for (size_t t = 0; t < rows.size(); ++t) {
+        const ConvRow& r = rows[t];
         v.push_back(make_int4(static_cast<int>(r.in1), static_cast<int>(r.in2), static_cast<int>(r.out),
-                              (produced.count(r.in1) ? 2 : 0) | (!r.copy && produced.count(r.in2) ? 4 : 0)));
+                              (produced.count(r.in1) ? 2 : 0) | (!r.copy && produced.count(r.in2) ? 4 : 0) |
+                                  (row_layer[t] << 8)));
+      }
       bw.jobs = dev_upload(v, stream);
     }
     const int warps = sms * L->band_blocks_per_sm(flow()) * (L->threads / 32);
@@ -610,6 +635,9 @@ struct Plan {
       cudaFree(w.flags);
     }
     cudaFree(flow_counter);
+    cudaFree(stamps);
+    cudaFree(peer_list);
+    cudaFree(peer_first);
     for (cudaEvent_t x : ev) cudaEventDestroy(x);
     for (void* p : owned) cudaFree(p);
     cudaFree(arena);
@@ -639,35 +667,48 @@ struct Plan {
            static_cast<int64_t>(batch) * nj * T * Q <= gr.prod_words;
   }
 
-  int launch_layer(int4* jobs, int nj, int batch, const ConvGroup& gr, cudaStream_t st) {
+  // ---- phase stamps (see Stamp in kernels.cuh): [0] conv start, [1 + L] end
+  // of graph conv layer L, then the tail's start, the scale end, the add
+  // layer ends and the extract end. Start slots hold inverted times.
+  Stamp* stamp_conv(int layer) const { return layer < 0 ? nullptr : stamps + 1 + layer; }
+  Stamp* stamp_tail_begin() const { return stamps + 1 + n_conv_layers; }
+  Stamp* stamp_scale() const { return stamps + 2 + n_conv_layers; }
+  Stamp* stamp_add(int layer) const { return stamps + 3 + n_conv_layers + layer; }
+  Stamp* stamp_extract() const { return stamps + 3 + n_conv_layers + n_add_layers; }
+  int nstamps() const { return 4 + n_conv_layers + n_add_layers; }
+
+  // layer: graph conv layer (-1 = a prologue fold layer, not stamped)
+  int launch_layer(int4* jobs, int nj, int batch, const ConvGroup& gr, cudaStream_t st, int layer) {
+    Stamp* b = layer < 0 ? nullptr : stamps;
     if (split_layer(nj, batch, gr)) {
-      SplitArgs a{arena, G, jobs, nj, batch, gr.prod, tri, T};
+      SplitArgs a{arena, G, jobs, nj, batch, gr.prod, tri, T, b, stamp_conv(layer)};
       L->conv_prod(a, st);
       L->conv_accum(a, st);
       return 2;
     }
-    ConvArgs a{arena, G, jobs, nj, (d + 2) / 2, batch};
+    ConvArgs a{arena, G, jobs, nj, (d + 2) / 2, batch, b, stamp_conv(layer)};
     L->conv(a, st);
     return 1;
   }
 
   // whole evaluation; a sharded plan (nranks > 1) runs only its conv share
   // here and the tail after the exchange (pse_plan_finish)
-  int launch_all(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
-    const int n = launch_conv(batch, marks);
-    return nranks > 1 ? n : n + launch_tail(batch, marks);
+  int launch_all(int batch) {
+    const int n = launch_conv(batch);
+    return nranks > 1 ? n : n + launch_tail(batch);
   }
 
-  int launch_conv(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
+  int launch_conv(int batch) {
     int launches = 0;
-    for (auto& [jobs, nj] : pro_layers) launches += launch_layer(jobs, nj, batch, groups[0], stream);
+    ck(cudaMemsetAsync(stamps, 0, sizeof(Stamp) * nstamps(), stream), "stamps");
+    for (auto& [jobs, nj] : pro_layers) launches += launch_layer(jobs, nj, batch, groups[0], stream, -1);
     const int first = band_first(batch);
     if (first > 0) {  // layered part: graph conv layers < first
       if (groups.size() == 1) {
         for (size_t q = 0; q < groups[0].layers.size(); ++q) {
-          if (groups[0].layer_index[q] >= first) continue;
-          launches += launch_layer(groups[0].layers[q].first, groups[0].layers[q].second, batch, groups[0], stream);
-          if (marks) mark(marks, 'c');
+          const int li = groups[0].layer_index[q];
+          if (li >= first) continue;
+          launches += launch_layer(groups[0].layers[q].first, groups[0].layers[q].second, batch, groups[0], stream, li);
         }
       } else {
         ck(cudaEventRecord(fork, stream), "fork");
@@ -675,11 +716,10 @@ struct Plan {
           ck(cudaStreamWaitEvent(gr.stream, fork, 0), "fork wait");
           for (size_t q = 0; q < gr.layers.size(); ++q)
             if (gr.layer_index[q] < first)
-              launches += launch_layer(gr.layers[q].first, gr.layers[q].second, batch, gr, gr.stream);
+              launches += launch_layer(gr.layers[q].first, gr.layers[q].second, batch, gr, gr.stream, gr.layer_index[q]);
           ck(cudaEventRecord(gr.join, gr.stream), "join");
           ck(cudaStreamWaitEvent(stream, gr.join, 0), "join wait");
         }
-        if (marks) mark(marks, 'c');
       }
     }
     if (first < static_cast<int>(layer_rows.size())) {  // banded part
@@ -687,48 +727,90 @@ struct Plan {
       if (flow()) {
         ck(cudaMemsetAsync(bw.flags, 0, sizeof(unsigned) * batch * bw.nunits, stream), "flags");
         ck(cudaMemsetAsync(flow_counter, 0, sizeof(unsigned long long), stream), "counter");
-        FlowArgs a{arena, G, bw.jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, bw.flags, flow_counter, bw.W};
+        FlowArgs a{arena, G, bw.jobs, bw.tasks, bw.dep_off, bw.deps, bw.nunits, batch, bw.flags, flow_counter, bw.W, stamps};
         L->conv_flow(a, sms * L->band_blocks_per_sm(true), stream);
         ++launches;
       } else {
         for (auto& [o, nw] : bw.waves) {
-          BandArgs a{arena, G, bw.jobs, bw.tasks + o * kSlots, nw, batch, bw.W};
+          BandArgs a{arena, G, bw.jobs, bw.tasks + o * kSlots, nw, batch, bw.W, stamps};
           L->conv_band(a, stream);
           ++launches;
         }
       }
-      if (marks) mark(marks, 'c');
     }
     return launches;
   }
 
   // term scales, addition layers, extraction
-  int launch_tail(int batch, std::vector<std::pair<char, cudaEvent_t>>* marks) {
+  int launch_tail(int batch) {
     int launches = 0;
+    Stamp* tb = stamp_tail_begin();
     if (nts) {
-      ScaleArgs a{arena, G, ts, nts, batch};
+      ScaleArgs a{arena, G, ts, nts, batch, tb, stamp_scale()};
       L->scale(a, stream);
       ++launches;
-      if (marks) mark(marks, 's');
     }
-    for (auto& [jobs, nj] : add_layers) {
-      AddArgs a{arena, G, jobs, nj, batch};
+    for (size_t q = 0; q < add_layers.size(); ++q) {
+      AddArgs a{arena, G, add_layers[q].first, add_layers[q].second, batch, tb, stamp_add(add_layer_index[q])};
       L->add(a, stream);
       ++launches;
-      if (marks) mark(marks, 'a');
     }
-    ExtractArgs e{arena, G, row_slot, row_mult, nrows, batch, vg};
+    ExtractArgs e{arena, G, row_slot, row_mult, nrows, batch, vg, tb, stamp_extract()};
     L->extract(e, stream);
     ++launches;
-    if (marks) mark(marks, 'e');
     return launches;
   }
 
-  void mark(std::vector<std::pair<char, cudaEvent_t>>* marks, char kind) {
-    const size_t i = marks->size();
-    ensure_events(static_cast<int>(i) + 2);
-    ck(cudaEventRecord(ev[i + 1], stream), "event");
-    marks->emplace_back(kind, ev[i + 1]);
+  // Phase times of the last run from the stamps (synchronous D2H of a few
+  // words). A phase ends when every job of it AND of the earlier phases is
+  // done (layers of independent monomials overlap on the device), so the
+  // per-layer times are non-negative and add up to the stage times. The
+  // reference's wall_ms covers the conv, scale and add phases
+  // (executor.cpp:168-183); the extraction is outside it, as there.
+  void read_stamps(pse_report* rep, bool tail) {
+    std::vector<Stamp> h(nstamps());
+    ck(cudaMemcpyAsync(h.data(), stamps, sizeof(Stamp) * h.size(), cudaMemcpyDeviceToHost, stream), "stamps D2H");
+    ck(cudaStreamSynchronize(stream), "stamps");
+    auto ms = [](Stamp a, Stamp b) { return b > a ? static_cast<double>(b - a) * 1e-6 : 0.0; };
+    const Stamp t0 = ~h[0];  // 0 (no conv kernel ran) -> ~0
+    Stamp at = h[0] ? t0 : 0;
+    conv_layer_ms.assign(n_conv_layers, 0.0);
+    for (int l = 0; l < n_conv_layers; ++l) {
+      const Stamp e = std::max(at, h[1 + l]);
+      conv_layer_ms[l] = at ? ms(at, e) : 0.0;
+      at = e;
+    }
+    const Stamp conv_end = at;
+    add_layer_ms.assign(n_add_layers, 0.0);
+    double scale = 0, add = 0;
+    Stamp tail_end = conv_end;
+    if (tail) {
+      // a sharded plan's tail starts after the exchange (barriers + gather);
+      // otherwise the launch gap belongs to the first tail phase
+      const Stamp tb = h[1 + n_conv_layers] ? ~h[1 + n_conv_layers] : conv_end;
+      at = nranks > 1 ? std::max(tb, conv_end) : conv_end;
+      exchange_ms = nranks > 1 ? ms(conv_end, at) : 0.0;
+      if (nts) {
+        const Stamp e = std::max(at, h[2 + n_conv_layers]);
+        scale = ms(at, e);
+        at = e;
+      }
+      for (int l = 0; l < n_add_layers; ++l) {
+        const Stamp e = std::max(at, h[3 + n_conv_layers + l]);
+        add_layer_ms[l] = ms(at, e);
+        add += add_layer_ms[l];
+        at = e;
+      }
+      tail_end = at;
+    }
+    if (rep) {
+      double conv = 0;
+      for (double x : conv_layer_ms) conv += x;
+      rep->conv_ms = conv;
+      rep->scale_ms = scale;
+      rep->add_ms = add;
+      rep->wall_ms = h[0] ? ms(t0, tail_end) : scale + add;
+    }
   }
 
   void ensure_events(int k) {
@@ -899,6 +981,12 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
     }
     p->layer_pairs = p->nrows_mine * ((g.d + 2) / 2) / std::max<int64_t>(1, nlayers);
     {
+      std::set<int64_t> outs;
+      for (const auto& lr : p->layer_rows)
+        for (const ConvRow& r : lr)
+          if (!outs.insert(r.out).second) p->multi_writer = true;
+    }
+    {
       const char* cm = getenv("PSE_CONV_MODE");
       const std::string m = cm ? cm : "";
       p->conv_mode = m == "layer" ? 1 : m == "band" ? 2 : m == "flow" ? 3 : 0;
@@ -949,7 +1037,11 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
     int2* dv = dev_upload(v, s);
     p->owned.push_back(dv);
     p->add_layers.emplace_back(dv, static_cast<int>(v.size()));
+    p->add_layer_index.push_back(L);
   }
+  p->n_conv_layers = g.n_conv_layers;
+  p->n_add_layers = g.n_add_layers;
+  p->stamps = dev_alloc<Stamp>(static_cast<size_t>(p->nstamps()));
   if (g.n_term_scales) {
     std::vector<int2> v;
     for (int64_t t = 0; t < g.n_term_scales; ++t) {
@@ -1088,31 +1180,36 @@ void exchange(Plan& p, int batch, int rank, double* buf) {
 }
 
 // copy every peer's addition-stage slots from its arena (peer_arena) into
-// ours; synchronous on the plan's stream
+// ours; synchronous on the plan's stream. The peer table is uploaded once
+// (and again only after a peer changes), so a gather is one kernel launch.
 void gather_peers(Plan& p, int batch) {
   if (p.nranks < 2) throw std::invalid_argument("plan is not sharded");
   if (batch < 1 || batch > p.max_batch) throw std::invalid_argument("batch outside [1, max_batch]");
   ck(cudaSetDevice(p.device), "cudaSetDevice");
-  std::vector<PeerList> peers;
-  std::vector<int64_t> first(1, 0);
-  for (int r = 0; r < p.nranks; ++r) {
-    if (r == p.rank || p.xslots[r].second == 0) continue;
-    if (r >= static_cast<int>(p.peer_arena.size()) || !p.peer_arena[r])
-      throw std::invalid_argument("peer arena of rank " + std::to_string(r) + " not set");
-    peers.push_back({p.peer_arena[r], p.xslots[r].first, p.xslots[r].second});
-    first.push_back(first.back() + static_cast<int64_t>(batch) * p.xslots[r].second * p.G.slot_words);
+  if (p.peers_dirty) {
+    std::vector<PeerList> peers;
+    std::vector<int64_t> first(1, 0);
+    for (int r = 0; r < p.nranks; ++r) {
+      if (r == p.rank || p.xslots[r].second == 0) continue;
+      if (r >= static_cast<int>(p.peer_arena.size()) || !p.peer_arena[r])
+        throw std::invalid_argument("peer arena of rank " + std::to_string(r) + " not set");
+      peers.push_back({p.peer_arena[r], p.xslots[r].first, p.xslots[r].second});
+      first.push_back(first.back() + static_cast<int64_t>(p.xslots[r].second) * p.G.slot_words);
+    }
+    ck(cudaStreamSynchronize(p.stream), "peer table");
+    cudaFree(p.peer_list);
+    cudaFree(p.peer_first);
+    p.peer_list = dev_upload(peers, p.stream);
+    p.peer_first = dev_upload(first, p.stream);
+    p.npeer_list = static_cast<int>(peers.size());
+    p.peer_words1 = first.back();
+    p.peers_dirty = false;
   }
-  if (peers.empty()) return;
-  PeerList* dpeers = dev_upload(peers, p.stream);
-  int64_t* dfirst = dev_upload(first, p.stream);
-  k_gather_peers<<<grid_for(first.back(), 256, p.sms), 256, 0, p.stream>>>(p.arena, p.G, dpeers,
-                                                                            static_cast<int>(peers.size()), dfirst, batch);
-  const cudaError_t e = cudaGetLastError();
-  const cudaError_t e2 = cudaStreamSynchronize(p.stream);
-  cudaFree(dpeers);
-  cudaFree(dfirst);
-  ck(e, "peer gather launch");
-  ck(e2, "peer gather");
+  if (p.npeer_list == 0) return;
+  k_gather_peers<<<grid_for(p.peer_words1 * batch, 256, p.sms), 256, 0, p.stream>>>(p.arena, p.G, p.peer_list,
+                                                                                   p.npeer_list, p.peer_first, batch);
+  ck(cudaGetLastError(), "peer gather launch");
+  ck(cudaStreamSynchronize(p.stream), "peer gather");
 }
 
 // the addition stage of a sharded plan once every rank's slots are in place
@@ -1123,7 +1220,7 @@ int finish(Plan& p, int batch, int detail, pse_report* rep) {
   p.ensure_events(2);
   (void)detail;
   ck(cudaEventRecord(p.ev[0], p.stream), "event");
-  const int launches = p.launch_tail(batch, nullptr);
+  const int launches = p.launch_tail(batch);
   ck(cudaEventRecord(p.ev[1], p.stream), "event");
   ck(cudaGetLastError(), "launch");
   ck(cudaEventSynchronize(p.ev[1]), "finish");
@@ -1131,70 +1228,48 @@ int finish(Plan& p, int batch, int detail, pse_report* rep) {
     std::memset(rep, 0, sizeof *rep);
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, p.ev[0], p.ev[1]), "elapsed");
-    rep->wall_ms = ms;
-    rep->add_ms = ms;
+    p.read_stamps(rep, true);
+    rep->device_ms = ms;
+    rep->exchange_ms = p.exchange_ms;
     rep->kernel_launches = launches;
     rep->batch = batch;
   }
   return PSE_OK;
 }
 
+// One evaluation of the resident arena: the whole phase sequence is captured
+// once per batch size into a CUDA graph and replayed. device_ms = CUDA events
+// on the plan's stream around the replay; the phase times come from the
+// kernels' own stamps of the same launches (read back when rep is given).
+// detail is accepted for compatibility: every run is stamped.
 int execute(Plan& p, int batch, int detail, pse_report* rep) {
+  (void)detail;
   if (batch < 1 || batch > p.max_batch) throw std::invalid_argument("batch outside [1, max_batch]");
   ck(cudaSetDevice(p.device), "cudaSetDevice");
   p.ensure_events(2);
   p.prepare_band(batch);
-  int launches = 0;
-  if (detail) {
-    std::vector<std::pair<char, cudaEvent_t>> marks;
-    ck(cudaEventRecord(p.ev[0], p.stream), "event");
-    launches = p.launch_all(batch, &marks);
-    ck(cudaGetLastError(), "launch");
-    ck(cudaEventSynchronize(marks.back().second), "execute");
-    if (rep) {
-      double conv = 0, scale = 0, add = 0, wall = 0;
-      cudaEvent_t prev = p.ev[0];
-      for (auto& [kind, e] : marks) {
-        float ms = 0;
-        ck(cudaEventElapsedTime(&ms, prev, e), "elapsed");
-        if (kind == 'c') conv += ms;
-        if (kind == 's') scale += ms;
-        if (kind == 'a') add += ms;
-        if (kind != 'e') wall += ms;
-        prev = e;
-      }
-      rep->conv_ms = conv;
-      rep->scale_ms = scale;
-      rep->add_ms = add;
-      rep->wall_ms = wall;
-    }
-  } else {
-    auto it = p.graphs.find(batch);
-    if (it == p.graphs.end()) {
-      cudaGraph_t graph;
-      ck(cudaStreamBeginCapture(p.stream, cudaStreamCaptureModeThreadLocal), "capture");
-      p.launch_all(batch, nullptr);
-      ck(cudaStreamEndCapture(p.stream, &graph), "capture end");
-      cudaGraphExec_t exec;
-      ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
-      cudaGraphDestroy(graph);
-      it = p.graphs.emplace(batch, exec).first;
-    }
-    ck(cudaEventRecord(p.ev[0], p.stream), "event");
-    ck(cudaGraphLaunch(it->second, p.stream), "graph launch");
-    ck(cudaEventRecord(p.ev[1], p.stream), "event");
-    ck(cudaEventSynchronize(p.ev[1]), "execute");
-    launches = p.kernel_count(batch);
-    if (rep) {
-      float ms = 0;
-      ck(cudaEventElapsedTime(&ms, p.ev[0], p.ev[1]), "elapsed");
-      rep->wall_ms = ms;
-      rep->conv_ms = rep->scale_ms = rep->add_ms = 0;
-    }
+  auto it = p.graphs.find(batch);
+  if (it == p.graphs.end()) {
+    cudaGraph_t graph;
+    ck(cudaStreamBeginCapture(p.stream, cudaStreamCaptureModeThreadLocal), "capture");
+    p.launch_all(batch);
+    ck(cudaStreamEndCapture(p.stream, &graph), "capture end");
+    cudaGraphExec_t exec;
+    ck(cudaGraphInstantiate(&exec, graph, 0), "instantiate");
+    cudaGraphDestroy(graph);
+    it = p.graphs.emplace(batch, exec).first;
   }
+  ck(cudaEventRecord(p.ev[0], p.stream), "event");
+  ck(cudaGraphLaunch(it->second, p.stream), "graph launch");
+  ck(cudaEventRecord(p.ev[1], p.stream), "event");
+  ck(cudaEventSynchronize(p.ev[1]), "execute");
   if (rep) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, p.ev[0], p.ev[1]), "elapsed");
+    p.read_stamps(rep, p.nranks == 1);
+    rep->device_ms = ms;
     fill_report(p, batch, rep);
-    rep->kernel_launches = launches;
+    rep->kernel_launches = p.kernel_count(batch);
   }
   return PSE_OK;
 }
@@ -1341,6 +1416,7 @@ static void set_peer(pse::Plan& P, int rank, const double* ptr, bool ipc) {
   if (P.peer_ipc[rank] && P.peer_arena[rank]) cudaIpcCloseMemHandle(const_cast<double*>(P.peer_arena[rank]));
   P.peer_arena[rank] = ptr;
   P.peer_ipc[rank] = ipc;
+  P.peers_dirty = true;
 }
 
 int pse_plan_open_peer(pse_plan* p, int32_t rank, const void* handle) {
@@ -1421,33 +1497,38 @@ int pse_plan_run(pse_plan* p, int32_t batch, const double* const* static_slabs, 
     if (!p) throw std::invalid_argument("null plan");
     pse::Plan& P = *p->p;
     pse::ck(cudaSetDevice(P.device), "cudaSetDevice");
-    cudaEvent_t e0, e1, e2, e3;
-    pse::ck(cudaEventCreate(&e0), "event");
-    pse::ck(cudaEventCreate(&e1), "event");
-    pse::ck(cudaEventCreate(&e2), "event");
-    pse::ck(cudaEventCreate(&e3), "event");
-    pse::ck(cudaEventRecord(e0, P.stream), "event");
+    P.ensure_events(6);  // ev[0..1]: execute; ev[2..5]: this call
+    pse::ck(cudaEventRecord(P.ev[2], P.stream), "event");
     pse::upload(P, batch, static_slabs, point_stride);
-    pse::ck(cudaEventRecord(e1, P.stream), "event");
+    pse::ck(cudaEventRecord(P.ev[3], P.stream), "event");
     pse_report r{};
     pse::execute(P, batch, 0, &r);
-    pse::ck(cudaEventRecord(e2, P.stream), "event");
+    pse::ck(cudaEventRecord(P.ev[4], P.stream), "event");
     pse::download(P, batch, value_grad_out, dyn_slabs_out);
-    pse::ck(cudaEventRecord(e3, P.stream), "event");
-    pse::ck(cudaEventSynchronize(e3), "run");
+    pse::ck(cudaEventRecord(P.ev[5], P.stream), "event");
+    pse::ck(cudaEventSynchronize(P.ev[5]), "run");
     float h2d = 0, d2h = 0, all = 0;
-    cudaEventElapsedTime(&h2d, e0, e1);
-    cudaEventElapsedTime(&d2h, e2, e3);
-    cudaEventElapsedTime(&all, e0, e3);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaEventDestroy(e2);
-    cudaEventDestroy(e3);
+    pse::ck(cudaEventElapsedTime(&h2d, P.ev[2], P.ev[3]), "elapsed");
+    pse::ck(cudaEventElapsedTime(&d2h, P.ev[4], P.ev[5]), "elapsed");
+    pse::ck(cudaEventElapsedTime(&all, P.ev[2], P.ev[5]), "elapsed");
     r.h2d_ms = h2d;
     r.d2h_ms = d2h;
     r.e2e_ms = all;
     r.kernel_launches += 1 + (dyn_slabs_out ? 1 : 0);
     if (rep) *rep = r;
+    return PSE_OK;
+  });
+}
+
+int pse_plan_layer_ms(const pse_plan* p, double* conv_layer_ms, int32_t n_conv, double* add_layer_ms, int32_t n_add) {
+  return pse::guarded([&] {
+    if (!p) throw std::invalid_argument("null plan");
+    const pse::Plan& P = *p->p;
+    if (n_conv != P.n_conv_layers || n_add != P.n_add_layers)
+      throw std::invalid_argument("layer counts do not match the plan's graph");
+    if ((n_conv && !conv_layer_ms) || (n_add && !add_layer_ms)) throw std::invalid_argument("null argument");
+    for (int l = 0; l < n_conv; ++l) conv_layer_ms[l] = l < static_cast<int>(P.conv_layer_ms.size()) ? P.conv_layer_ms[l] : 0.0;
+    for (int l = 0; l < n_add; ++l) add_layer_ms[l] = l < static_cast<int>(P.add_layer_ms.size()) ? P.add_layer_ms[l] : 0.0;
     return PSE_OK;
   });
 }

@@ -26,6 +26,28 @@ struct Geom {
   int64_t point_words;// device slots * Q * S
 };
 
+// Phase stamps (RunReport per-layer times, executor.hpp:31-43): kernels
+// record %globaltimer into a per-plan array with atomics -- a phase's start as
+// atomicMax of the inverted time (so one zero-fill resets every slot), its end
+// as atomicMax of the time -- see Plan::read_stamps in engine.cu.
+using Stamp = unsigned long long;
+__device__ __forceinline__ Stamp global_ns() {
+  Stamp t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// one atomic per block at entry: the phase cannot start before this
+__device__ __forceinline__ void stamp_begin(Stamp* s) {
+  if (s && threadIdx.x == 0) atomicMax(s, ~global_ns());
+}
+// one atomic per converged group of lanes on the way out
+__device__ __forceinline__ void stamp_finish(Stamp* s) {
+  if (s) {
+    const unsigned mask = __activemask();
+    if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(mask) - 1)) atomicMax(s, global_ns());
+  }
+}
+
 struct ConvArgs {
   double* arena;
   Geom G;
@@ -33,6 +55,8 @@ struct ConvArgs {
   int njobs;
   int npairs;        // coefficient pairs per job: (d+2)/2
   int batch;
+  Stamp* t_begin;    // conv stage start (inverted), or null
+  Stamp* t_end;      // this layer's end, or null
 };
 
 struct AddArgs {
@@ -41,6 +65,8 @@ struct AddArgs {
   const int2* jobs;  // (src, dst): dst := dst + src
   int njobs;
   int batch;
+  Stamp* t_begin;    // tail start (inverted), or null
+  Stamp* t_end;
 };
 
 struct ScaleArgs {
@@ -49,6 +75,8 @@ struct ScaleArgs {
   const int2* items;  // (slot, factor) -- factors are small exact integers
   int nitems;
   int batch;
+  Stamp* t_begin;
+  Stamp* t_end;
 };
 
 struct ExtractArgs {
@@ -59,6 +87,8 @@ struct ExtractArgs {
   int nrows;
   int batch;
   double* out;           // [Q][batch][nrows][d+1]
+  Stamp* t_begin;
+  Stamp* t_end;
 };
 
 struct MdArgs {
@@ -84,6 +114,8 @@ struct SplitArgs {
   double* prod;          // scratch: [point][job][T][Q], T = (d+1)(d+2)/2
   const int2* tri;       // [T] (k, i) of triangular product index k(k+1)/2 + i
   int T;
+  Stamp* t_begin;
+  Stamp* t_end;
 };
 
 // Banded convolution (deep graphs, few jobs per layer). A conv job's output
@@ -114,11 +146,13 @@ struct BandArgs {
   double* arena;
   Geom G;
   const int4* jobs;   // (in1, in2, out, flags) of every banded conv job;
-                      // flags: 2 = in1 and 4 = in2 produced by a conv job
+                      // flags: 2 = in1 and 4 = in2 produced by a conv job,
+                      // bits 8+ = the job's graph conv layer
   const int4* tasks;  // kSlots slots per warp descriptor, one wave
   int ntasks;         // warp descriptors
   int batch;
   int W;              // band width
+  Stamp* stamps;      // [0] conv start (inverted), [1 + layer] layer ends; or null
 };
 
 struct FlowArgs {
@@ -133,6 +167,7 @@ struct FlowArgs {
   unsigned* flags;      // [batch][nunits], zero before the launch
   unsigned long long* counter;  // zero before the launch
   int W;                // band width
+  Stamp* stamps;        // as BandArgs
 };
 
 struct Launchers {
@@ -221,13 +256,8 @@ constexpr int conv_default_minb() {
   return 4;
 }
 
-template <int M, bool CPLX, int MINB>
-__global__ void __launch_bounds__(kConvThreads, blocks_for(MINB)) k_conv(const ConvArgs a) {
-  extern __shared__ double smem[];
-  const Lane sm = make_lane(smem);
-  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * a.npairs;
-  if (g >= ntasks) return;
+template <int M, bool CPLX>
+__device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm) {
   const int pair = static_cast<int>(g % a.npairs);
   const int64_t r = g / a.npairs;
   const int jb = static_cast<int>(r % a.njobs);
@@ -322,6 +352,15 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(MINB)) k_conv(const C
       if (i == kk) store_md<M>(Z + M * S, S, kk, ai);
     }
   }
+}
+
+template <int M, bool CPLX, int MINB>
+__global__ void __launch_bounds__(kConvThreads, blocks_for(MINB)) k_conv(const ConvArgs a) {
+  extern __shared__ double smem[];
+  stamp_begin(a.t_begin);
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < static_cast<int64_t>(a.batch) * a.njobs * a.npairs) conv_pair<M, CPLX>(a, g, make_lane(smem));
+  stamp_finish(a.t_end);
 }
 
 // ------------------------------------------------- banded convolution (deep)
@@ -539,15 +578,30 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
   }
 }
 
+// end stamps of the layers of one warp descriptor's tasks (lane 0)
+__device__ __forceinline__ void stamp_tasks(Stamp* stamps, const int4* __restrict__ jobs, const int4* __restrict__ slots) {
+  if (!stamps) return;
+  const Stamp now = global_ns();
+#pragma unroll 1
+  for (int f = 0; f < kSlots; ++f) {
+    const int4 T = slots[f];
+    if (T.w != -4 && (f == 0 || slots[f - 1].x != T.x || slots[f - 1].y != T.y || slots[f - 1].z != T.z))
+      atomicMax(stamps + 1 + (jobs[T.x].w >> 8), now);
+  }
+}
+
 template <int M, bool CPLX>
 __global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_band(const BandArgs a) {
   extern __shared__ double smem[];
   const Lane sm = make_lane(smem);
+  if (a.stamps) stamp_begin(a.stamps);
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (gw >= static_cast<int64_t>(a.batch) * a.ntasks) return;
   const int tw = static_cast<int>(gw % a.ntasks);
-  band_task<M, CPLX, false>(a.arena, a.G, a.jobs, a.tasks + static_cast<int64_t>(tw) * kSlots, a.W, gw / a.ntasks,
-                            threadIdx.x & 31, sm, nullptr);
+  const int4* slots = a.tasks + static_cast<int64_t>(tw) * kSlots;
+  band_task<M, CPLX, false>(a.arena, a.G, a.jobs, slots, a.W, gw / a.ntasks, threadIdx.x & 31, sm, nullptr);
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) stamp_tasks(a.stamps, a.jobs, slots);
 }
 
 // Dataflow form of the banded convolution: ONE persistent launch. Warps take
@@ -578,6 +632,7 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_flow(const
   constexpr int Q = CPLX ? 2 * M : M;
   double* stg = smem + kLaneThreads * (CPLX && !cplx_acc_lane<M>() ? MdTraits<M>::LANE : MdTraits<M>::LANE_CONV) +
                 (threadIdx.x >> 5) * kStageSlots * Q;
+  if (a.stamps) stamp_begin(a.stamps);
   for (;;) {
     unsigned long long u = 0;
     if (lane == 0) u = atomicAdd(a.counter, 1ull);
@@ -608,7 +663,10 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_flow(const
     __syncwarp();  // the staging area is rewritten by the next unit
     __threadfence();
     __syncwarp();
-    if (lane == 0) st_release(fl + p, 1u);
+    if (lane == 0) {
+      st_release(fl + p, 1u);
+      stamp_tasks(a.stamps, a.jobs, a.tasks + static_cast<int64_t>(p) * kSlots);
+    }
   }
 }
 
@@ -617,12 +675,7 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_flow(const
 // complex coefficient pair is the (re, im) pair conv() adds to its
 // accumulators: sub(mul(re,re), mul(im,im)), add(mul(re,im), mul(im,re)).
 template <int M, bool CPLX>
-__global__ void __launch_bounds__(kConvThreads) k_conv_prod(const SplitArgs a) {
-  extern __shared__ double smem[];
-  const Lane sm = make_lane(smem);
-  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * a.T;
-  if (g >= ntasks) return;
+__device__ __forceinline__ void conv_prod_item(const SplitArgs& a, int64_t g, Lane sm) {
   const int off = static_cast<int>(g % a.T);
   const int64_t r = g / a.T;
   const int jb = static_cast<int>(r % a.njobs);
@@ -660,16 +713,19 @@ __global__ void __launch_bounds__(kConvThreads) k_conv_prod(const SplitArgs a) {
   }
 }
 
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kConvThreads) k_conv_prod(const SplitArgs a) {
+  extern __shared__ double smem[];
+  stamp_begin(a.t_begin);
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < static_cast<int64_t>(a.batch) * a.njobs * a.T) conv_prod_item<M, CPLX>(a, g, make_lane(smem));
+}
+
 // Phase B: one thread per (point, job, coefficient pair), the same pairing
 // as k_conv; acc = P(k,0), acc = md_add(acc, P(k,i)) for ascending i.
 template <int M, bool CPLX>
-__global__ void __launch_bounds__(kConvThreads) k_conv_accum(const SplitArgs a) {
-  extern __shared__ double smem[];
-  const Lane sm = make_lane(smem);
+__device__ __forceinline__ void conv_accum_pair(const SplitArgs& a, int64_t g, Lane sm) {
   const int npairs = (a.G.d + 2) / 2;
-  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * npairs;
-  if (g >= ntasks) return;
   const int pair = static_cast<int>(g % npairs);
   const int64_t r = g / npairs;
   const int jb = static_cast<int>(r % a.njobs);
@@ -729,17 +785,20 @@ __global__ void __launch_bounds__(kConvThreads) k_conv_accum(const SplitArgs a) 
   }
 }
 
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kConvThreads) k_conv_accum(const SplitArgs a) {
+  extern __shared__ double smem[];
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < static_cast<int64_t>(a.batch) * a.njobs * ((a.G.d + 2) / 2)) conv_accum_pair<M, CPLX>(a, g, make_lane(smem));
+  stamp_finish(a.t_end);
+}
+
 // ---------------------------------------------------------------- addition
 // One thread per (point, job, coefficient): dst_k := md_add(dst_k, src_k)
 // (executor.cpp:144-148, operand order x = dst, y = src).
 template <int M, bool CPLX>
-__global__ void __launch_bounds__(kAddThreads) k_add(const AddArgs a) {
-  extern __shared__ double smem[];
-  const Lane sm = make_lane(smem);
+__device__ __forceinline__ void add_item(const AddArgs& a, int64_t g, Lane sm) {
   const int d1 = a.G.d + 1;
-  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.njobs * d1;
-  if (g >= ntasks) return;
   const int k = static_cast<int>(g % d1);
   const int64_t r = g / d1;
   const int jb = static_cast<int>(r % a.njobs);
@@ -759,16 +818,20 @@ __global__ void __launch_bounds__(kAddThreads) k_add(const AddArgs a) {
   }
 }
 
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kAddThreads) k_add(const AddArgs a) {
+  extern __shared__ double smem[];
+  stamp_begin(a.t_begin);
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < static_cast<int64_t>(a.batch) * a.njobs * (a.G.d + 1)) add_item<M, CPLX>(a, g, make_lane(smem));
+  stamp_finish(a.t_end);
+}
+
 // ------------------------------------------------------------ scale phase
 // TermScale (executor.cpp:138-143 -> series_scale_int, pseries.cpp:85-93)
 template <int M, bool CPLX>
-__global__ void __launch_bounds__(kAddThreads) k_scale(const ScaleArgs a) {
-  extern __shared__ double smem[];
-  const Lane sm = make_lane(smem);
+__device__ __forceinline__ void scale_item(const ScaleArgs& a, int64_t g, Lane sm) {
   const int d1 = a.G.d + 1;
-  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.nitems * d1;
-  if (g >= ntasks) return;
   const int k = static_cast<int>(g % d1);
   const int64_t r = g / d1;
   const int it = static_cast<int>(r % a.nitems);
@@ -788,17 +851,21 @@ __global__ void __launch_bounds__(kAddThreads) k_scale(const ScaleArgs a) {
   }
 }
 
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kAddThreads) k_scale(const ScaleArgs a) {
+  extern __shared__ double smem[];
+  stamp_begin(a.t_begin);
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < static_cast<int64_t>(a.batch) * a.nitems * (a.G.d + 1)) scale_item<M, CPLX>(a, g, make_lane(smem));
+  stamp_finish(a.t_end);
+}
+
 // ----------------------------------------------------------------- extract
 // extract (executor.cpp:254-269): value row then one row per variable,
 // multiplier applied with md_mul, absent variables give zero series.
 template <int M, bool CPLX>
-__global__ void __launch_bounds__(kAddThreads) k_extract(const ExtractArgs a) {
-  extern __shared__ double smem[];
-  const Lane sm = make_lane(smem);
+__device__ __forceinline__ void extract_item(const ExtractArgs& a, int64_t g, Lane sm) {
   const int d1 = a.G.d + 1;
-  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t ntasks = static_cast<int64_t>(a.batch) * a.nrows * d1;
-  if (g >= ntasks) return;
   const int k = static_cast<int>(g % d1);
   const int64_t r = g / d1;
   const int row = static_cast<int>(r % a.nrows);
@@ -828,6 +895,15 @@ __global__ void __launch_bounds__(kAddThreads) k_extract(const ExtractArgs a) {
 #pragma unroll
     for (int q = 0; q < M; ++q) out[(part * M + q) * plane] = x[q];
   }
+}
+
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kAddThreads) k_extract(const ExtractArgs a) {
+  extern __shared__ double smem[];
+  stamp_begin(a.t_begin);
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g < static_cast<int64_t>(a.batch) * a.nrows * (a.G.d + 1)) extract_item<M, CPLX>(a, g, make_lane(smem));
+  stamp_finish(a.t_end);
 }
 
 // --------------------------------------------------------- md primitives

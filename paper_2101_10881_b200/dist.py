@@ -97,28 +97,29 @@ def evaluate_sharded(plan, batch: int = 1, detail: bool = True, p2p: bool = Fals
     is either the peer gather (p2p, after connect_peers: every rank reads the
     slots it lacks straight from the peers' arenas, between two barriers) or
     an all-gather of packed blocks (NCCL over NVLink on GPUs, gloo through
-    host memory when several ranks share a device). Returns (conv_ms,
-    exchange_ms, finish_ms)."""
-    import time
+    host memory when several ranks share a device).
 
+    Returns (conv_report, finish_report). The finish report's times come from
+    the kernels' %globaltimer stamps on this rank's device: conv_ms (the conv
+    stage), exchange_ms (conv end -> first addition-stage kernel: the barriers
+    and the gather), add_ms, and wall_ms (conv start -> last addition layer)."""
     import torch
     import torch.distributed as dist
 
     world = plan.nranks
     dev = torch.device(f"cuda:{plan.device}")
-    rep = plan.execute(batch, detail=detail)  # returns once the conv stage has finished
+    rep = plan.execute(batch)  # returns once the conv stage has finished
     if p2p and world > 1:
-        t0 = time.perf_counter()
         dist.barrier()  # every rank's term slots are final
         plan.gather_peers(batch)
         dist.barrier()  # every rank has read ours before our addition tree rewrites them
-        ex_ms = (time.perf_counter() - t0) * 1e3
-        fin = plan.finish(batch)
-        return rep.conv_ms, ex_ms, fin.wall_ms
+        return rep, plan.finish(batch)
     words = [plan.exchange_words(r, batch) for r in range(world)]
     width = max(1, max(words))
     mine = torch.zeros(width, dtype=torch.float64, device=dev)
-    t0 = time.perf_counter()
+    # the zero-fill runs on torch's stream, pack on the plan's non-blocking
+    # stream: order them (otherwise the fill may land after the packed slots)
+    torch.cuda.current_stream(dev).synchronize()
     plan.pack(mine.data_ptr(), batch)
     on_gpu = dist.is_initialized() and dist.get_backend() == "nccl"
     if world == 1 or not dist.is_initialized():
@@ -132,12 +133,11 @@ def evaluate_sharded(plan, batch: int = 1, detail: bool = True, p2p: bool = Fals
         outs = [torch.empty_like(host) for _ in range(world)]
         dist.all_gather(outs, host)
         blocks = [o.to(dev) for o in outs]
+        torch.cuda.synchronize(dev)
     for r in range(world):
         if r != plan.rank:
             plan.unpack(r, blocks[r].data_ptr(), batch)
-    ex_ms = (time.perf_counter() - t0) * 1e3
-    fin = plan.finish(batch)
-    return rep.conv_ms, ex_ms, fin.wall_ms
+    return rep, plan.finish(batch)
 
 
 def gather_points(local, total: int, device=None):

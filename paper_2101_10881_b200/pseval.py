@@ -371,6 +371,9 @@ class RunReport:
     conv_jobs_executed: int = 0
     add_jobs_executed: int = 0
     kernel_launches: int = 0
+    conv_layer_ms: List[float] = field(default_factory=list)  # executor.hpp:31-43
+    add_layer_ms: List[float] = field(default_factory=list)
+    device_ms: float = 0.0
 
 
 def _split_vg(vg: np.ndarray, P: int, m: int, n: int, d: int):
@@ -486,9 +489,19 @@ class DevicePlan:
         check(lib().pse_plan_execute(self._h, batch, int(detail), C.byref(rep)))
         return rep
 
-    def download(self, batch: int = 1, want_dyn: bool = False):
+    def layer_ms(self):
+        """(conv_layer_ms, add_layer_ms) of the last run (pse_plan_layer_ms;
+        RunReport's per-phase lists, executor.cpp:154-157)"""
+        nc, na = int(self._desc.n_conv_layers), int(self._desc.n_add_layers)
+        c, a = np.zeros(nc), np.zeros(na)
+        check(lib().pse_plan_layer_ms(self._h, ptr(c), nc, ptr(a), na))
+        return [float(x) for x in c], [float(x) for x in a]
+
+    def download(self, batch: int = 1, want_dyn: bool = False, out: Optional[np.ndarray] = None):
+        """(vg [Q][batch][n+1][d+1], dyn or None); out: a caller-owned
+        (e.g. pinned) C-contiguous array of vg's shape to write into"""
         n, d = self.graph.n, self.graph.d
-        vg = np.empty((self.Q, batch, n + 1, d + 1), np.float64)
+        vg = out if out is not None else np.empty((self.Q, batch, n + 1, d + 1), np.float64)
         vw = batch * (n + 1) * (d + 1)
         vptr = ptr_array([vg.ctypes.data + q * vw * 8 for q in range(self.Q)])
         dyn, dptr = None, None
@@ -537,7 +550,9 @@ def run_device(g: JobGraph, a: DataArray, device: int = 0) -> RunReport:
         a.slabs[...] = dyn
         P = 2 if a.mode == CPLX else 1
         value, grad = _split_vg(vg, P, a.m, n, d)
-        return _report(value, grad, rep)
+        out = _report(value, grad, rep)
+        out.conv_layer_ms, out.add_layer_ms = plan.layer_ms()
+        return out
     finally:
         plan.close()
 
@@ -545,7 +560,7 @@ def run_device(g: JobGraph, a: DataArray, device: int = 0) -> RunReport:
 def _report(value, grad, rep: Report) -> RunReport:
     return RunReport(value, grad, rep.wall_ms, rep.conv_ms, rep.add_ms, rep.scale_ms, rep.h2d_ms, rep.d2h_ms,
                      rep.e2e_ms, int(rep.double_op_count), int(rep.alg_op_count), int(rep.conv_jobs_executed),
-                     int(rep.add_jobs_executed), int(rep.kernel_launches))
+                     int(rep.add_jobs_executed), int(rep.kernel_launches), device_ms=rep.device_ms)
 
 
 def evaluate_packed(n: int, d: int, m: int, mode: str, nvars, indices, exponents, stat: np.ndarray,

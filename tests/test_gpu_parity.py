@@ -261,6 +261,67 @@ def test_benchmark_configs_full_size_bitwise_vs_reference_engine(cfg, pid, m):
     assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"{cfg}: {pid} d=152 m={m} ({plan.conv_path(1)})")
 
 
+def _c5_wave_as_benched(d, m, total, first, batch):
+    """C5 exactly as bench.py stages it: the static blocks of points
+    [0, total) (coefficients of seed 7, point b's z from seed 1000+b,
+    bench.make_static) resident in HBM as one CUDA tensor, points
+    [first, first+batch) staged into the plan by DevicePlan.upload_ptr (a D2D
+    copy out of the middle of the buffer), then the captured-graph replay
+    the timed steps use. Returns (stat [Q][total][top][d+1], plan, vg of the
+    wave)."""
+    import torch
+
+    import bench
+
+    n, N, nvars, idx, stat = bench.make_static("p2h", d, m, range(total))
+    g = pe.build_jobgraph_shape(n, d, nvars, idx)
+    plan = pe.DevicePlan(g, m, "real", 0, batch)
+    stat_dev = torch.from_numpy(np.ascontiguousarray(stat)).to("cuda:0")
+    torch.cuda.synchronize()
+    plan.upload_ptr(stat_dev.data_ptr(), batch, total=total, first=first)
+    plan.execute(batch, detail=False)
+    vg, _ = plan.download(batch)
+    return (n, N, nvars, idx, stat), plan, vg
+
+
+@pytest.mark.timeout(1200)
+def test_c5_wave_as_benched_bitwise():
+    """BASELINE C5 (p2h, d=152, m=10, point b's inputs from seed 1000+b,
+    gen.cpp:50-71) through the bench's own staging path: a 16-point wave
+    taken from the middle of a 40-point device buffer (first=9, total=40)
+    equals each point evaluated alone on the device, and points of the wave
+    equal the reference engine (oracle/_ref run_parallel) bit for bit."""
+    import os
+
+    d, m, total, first, batch = 152, 10, 40, 9, 16
+    (n, N, nvars, idx, stat), plan, vg = _c5_wave_as_benched(d, m, total, first, batch)
+    assert plan.conv_path(batch) in ("layered", "hybrid", "dataflow")
+    g = plan.graph
+    single = pe.DevicePlan(g, m, "real", 0, 1)
+    for b in range(batch):
+        one, _, _ = single.run(np.ascontiguousarray(stat[:, first + b]), 1)
+        assert_bitwise(vg[:, b], one[:, 0], f"C5 wave point {first + b} vs single-point run")
+    if not po.has_ref():
+        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
+    for b in (0, batch - 1):
+        p = po.Problem(n, d, m, False, nvars, idx, None, stat[:, first + b].reshape(1, m, -1, d + 1))
+        ref = po.evaluate(p, "ref", workers=os.cpu_count() or 1)
+        assert_bitwise(vg[:, b].reshape(ref.shape), ref, f"C5 point {first + b} vs reference engine")
+
+
+@pytest.mark.timeout(1200)
+def test_c5_grid_of_128_points_bitwise():
+    """The grid size C5 runs at (waves of 128 points in one launch per
+    layer), on a smaller degree: a 128-point wave at offset 3 of a 140-point
+    device buffer equals the C oracle point by point."""
+    d, m, total, first, batch = 20, 3, 140, 3, 128
+    (n, N, nvars, idx, stat), plan, vg = _c5_wave_as_benched(d, m, total, first, batch)
+    for b in list(range(0, batch, 9)) + [batch - 1]:
+        p = po.Problem(n, d, m, False, nvars, idx, None, stat[:, first + b].reshape(1, m, -1, d + 1))
+        ref = po.evaluate(p, "port")
+        assert_bitwise(vg[:, b].reshape(ref.shape), ref, f"128-point wave, point {first + b}")
+
+
 @pytest.mark.parametrize("pid,d,m", [("p1", 64, 4), ("p2", 40, 2), ("p1", 152, 10)])
 def test_complex_benchmark_graphs_bitwise_vs_reference_engine(pid, d, m):
     """Complex mode (separate re/im slabs, the complex conv of pseries.cpp:49-59)
@@ -303,6 +364,7 @@ def test_reference_binding_drop_in():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK: 4/4" in r.stdout
+    assert "OK: RunReport per-layer timings" in r.stdout, r.stdout
 
 
 @pytest.mark.parametrize("pid,d,m,nranks", [("p1", 15, 2, 2), ("p1", 8, 4, 3), ("p3", 4, 2, 4), ("p2", 3, 3, 2)])
@@ -324,6 +386,7 @@ def test_monomial_sharding_is_bit_exact(pid, d, m, nranks):
         p.upload(pr.stat, 1)
         p.execute(1, detail=True)
         buf = torch.zeros(width, dtype=torch.float64, device="cuda:0")
+        torch.cuda.synchronize()  # the fill (torch's stream) before pack (the plan's stream)
         p.pack(buf.data_ptr())
         blocks.append(buf)
     assert sum(plans[0].exchange_words(r) for r in range(nranks)) > 0
@@ -459,3 +522,90 @@ def test_cli_verify_and_bench(tmp_path):
     assert "| p1 | 15 | 2 | real |" in r.stdout
     rows = open(csv).read().strip().split("\n")
     assert rows[0].startswith("id,d,m,mode,workers") and len(rows) == 3
+
+
+def test_slot_rewritten_in_a_later_layer_stays_exact():
+    """validate() (jobgraph.cpp:273-336) accepts a dynamic slot written again
+    in a later conv layer. The banded/dataflow schedule assumes one producer
+    per slot, so the planner keeps such graphs on the layered path (with the
+    dataflow path forced, too). The result equals the same graph with the
+    rewrite sent to a fresh slot and the addition stage reading that slot."""
+    import os
+
+    pr = pe.gen_benchmark("p1", 6, 2, seed=7)
+    g = pe.build_jobgraph_shape(pr.n, pr.d, pr.nvars, pr.indices)
+    top = 1 + g.N + g.n
+    F = int(next(s for s in g.add_src if s >= top))  # a dynamic term slot the addition stage reads
+    z1, z2 = top - g.n, top - g.n + 1  # two input slots
+    off = list(g.conv_layer_off) + [g.conv_layer_off[-1] + 1]
+
+    def graph_with_rewrite(out, total, add_src, add_dst, value_slot, grads):
+        return pe.GraphArrays(g.n, g.N, g.d, total, value_slot, grads, g.multipliers, off,
+                              list(g.conv_in1) + [z1], list(g.conv_in2) + [z2], list(g.conv_out) + [out],
+                              list(g.conv_copy) + [0], g.add_layer_off, add_src, add_dst)
+
+    multi = graph_with_rewrite(F, g.total_slots, g.add_src, g.add_dst, g.value_slot, g.gradient_slots)
+    assert pe.validate(multi)[0]
+    Fp = g.total_slots  # the renamed twin: the rewrite goes to a fresh slot
+    ren = lambda a: [Fp if int(s) == F else int(s) for s in a]
+    renamed = graph_with_rewrite(Fp, g.total_slots + 1, ren(g.add_src), ren(g.add_dst),
+                                 ren([g.value_slot])[0], ren(g.gradient_slots))
+    assert pe.validate(renamed)[0]
+    st = pr.stat.reshape(2, 1, *pr.stat.shape[1:])[:, 0]
+    want, _, _ = pe.DevicePlan(renamed, 2, "real", 0, 1).run(st, 1)
+    for mode in ("", "flow"):
+        if mode:
+            os.environ["PSE_CONV_MODE"] = mode
+        try:
+            plan = pe.DevicePlan(multi, 2, "real", 0, 1)
+            assert plan.conv_path(1) == "layered"
+            got, _, _ = plan.run(st, 1)
+        finally:
+            os.environ.pop("PSE_CONV_MODE", None)
+        assert_bitwise(got, want, f"rewritten slot (PSE_CONV_MODE={mode or 'auto'})")
+
+
+@pytest.mark.parametrize("mode", ["", "layer", "flow"])
+def test_run_report_per_layer_times(mode, monkeypatch):
+    """RunReport's per-phase lists (executor.hpp:31-43, executor.cpp:154-157)
+    from the kernels' own stamps, through run_device: one entry per conv and
+    per add layer, non-negative, summing to conv_ms / add_ms, and with the
+    scale phase to wall_ms; the graph-replay path reports them too."""
+    if mode:
+        monkeypatch.setenv("PSE_CONV_MODE", mode)
+    pr = pe.gen_benchmark("p1", 40, 3, seed=7)
+    g = pe.build_jobgraph_shape(pr.n, pr.d, pr.nvars, pr.indices)
+    poly, z = pr.polynomial()
+    a = pe.stage(poly, z)
+    r = pe.run_device(g, a)
+    assert len(r.conv_layer_ms) == len(g.conv_layer_sizes()) and len(r.add_layer_ms) == len(g.add_layer_sizes())
+    assert min(r.conv_layer_ms) >= 0 and min(r.add_layer_ms) >= 0
+    assert r.conv_ms > 0 and r.add_ms > 0
+    assert abs(sum(r.conv_layer_ms) - r.conv_ms) <= 1e-9 + 1e-6 * r.conv_ms
+    assert abs(sum(r.add_layer_ms) - r.add_ms) <= 1e-9 + 1e-6 * r.add_ms
+    assert abs(r.conv_ms + r.scale_ms + r.add_ms - r.wall_ms) <= 1e-6 * r.wall_ms
+    assert r.device_ms >= r.wall_ms * 0.99
+    plan = pe.DevicePlan(g, 3, "real", 0, 1)
+    plan.upload(pr.stat, 1)
+    for _ in range(2):
+        rep = plan.execute(1)
+        assert rep.conv_ms > 0 and rep.add_ms > 0 and rep.device_ms >= rep.wall_ms * 0.99
+
+
+def test_sharded_report_times_the_exchange_on_the_device():
+    """a sharded plan's finish report: conv stage, exchange (conv end ->
+    addition-stage start), additions, all from the device's own clock"""
+    pr = pe.gen_benchmark("p1", 15, 2, seed=7)
+    g = pe.build_jobgraph_shape(pr.n, pr.d, pr.nvars, pr.indices)
+    plans = [pe.DevicePlan(g, 2, "real", 0, 1, rank=r, nranks=2) for r in range(2)]
+    plans[0].set_peer(1, plans[1])
+    plans[1].set_peer(0, plans[0])
+    for p in plans:
+        p.upload(pr.stat, 1)
+        p.execute(1)
+    for p in plans:
+        p.gather_peers(1)
+    for p in plans:
+        fin = p.finish(1)
+        assert fin.conv_ms > 0 and fin.add_ms > 0 and fin.exchange_ms >= 0
+        assert abs(fin.conv_ms + fin.exchange_ms + fin.scale_ms + fin.add_ms - fin.wall_ms) <= 1e-6 * fin.wall_ms + 1e-6
