@@ -303,6 +303,7 @@ CONV_KERNEL = {
     "waves": "k_conv_band<{m},real> (one launch per scheduled wave of band x segment tasks)",
     "dataflow": "k_conv_flow<{m},real> (one persistent launch per evaluation wave)",
     "hybrid": "k_conv<{m},real> for the large conv layers, then k_conv_flow<{m},real> for the trailing small ones",
+    "cta": "k_conv_cta<{m},real> (one block per independent job group and point, CTA-local dataflow)",
 }
 
 

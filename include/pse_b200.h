@@ -27,6 +27,9 @@
  *   pse_md_apply                          <- md_add / md_sub / md_mul (multidouble.hpp:75-94 ->
  *                                            expansion.hpp:142-211), elementwise on arrays
  *   pse_series_conv                       <- Series conv(const Series&, const Series&)  src/pseries.cpp:37-64
+ *   pse_eval_direct                       <- Evaluation eval_direct(const Polynomial&, const std::vector<Series>&)
+ *                                            include/pseval/oracle.hpp, src/oracle_direct.cpp:41-78
+ *   pse_plan_layer_ms                     <- RunReport::conv_layer_ms / add_layer_ms  executor.hpp:31-43
  *
  * Array conventions (P = 2 parts re/im in complex mode, else 1; Q = P*m slabs;
  * slab q = part*m + limb, exactly the reference DataArray's re[0..m-1] then
@@ -216,8 +219,9 @@ int pse_plan_stream(const pse_plan* p, void** stream);
  * PSE_CONV_WAVES (band x segment tasks, one launch per scheduled wave),
  * PSE_CONV_DATAFLOW (the same tasks in one persistent launch) or
  * PSE_CONV_HYBRID (layered for the large layers, then one dataflow launch
- * for the trailing small ones) */
-enum { PSE_CONV_LAYERED = 1, PSE_CONV_WAVES = 2, PSE_CONV_DATAFLOW = 3, PSE_CONV_HYBRID = 4 };
+ * for the trailing small ones) or PSE_CONV_CTA (one block per independent job
+ * group and point, the group's band tasks synchronised in shared memory) */
+enum { PSE_CONV_LAYERED = 1, PSE_CONV_WAVES = 2, PSE_CONV_DATAFLOW = 3, PSE_CONV_HYBRID = 4, PSE_CONV_CTA = 5 };
 int pse_plan_conv_path(const pse_plan* p, int32_t batch, int32_t* path);
 /* host only (no device): the banded task schedule of a whole graph with band
  * width W (16 or 32), in dataflow order (flow != 0) or waves of `procs` warps;
@@ -234,6 +238,20 @@ int pse_band_schedule_stats(const pse_graph_desc* desc, int32_t W, int32_t flow,
 int pse_evaluate(int32_t n, int32_t d, int32_t m, int32_t mode, int32_t N, const int32_t* nvars,
                  const int32_t* indices, const int32_t* exponents, int32_t batch, const double* stat,
                  double* vg_out, int32_t device, pse_report* rep);
+
+/* eval_direct (oracle_direct.cpp:41-78) on the device: the INDEPENDENT
+ * evaluator `verify` checks the engine against (proj/tools/pseval.cpp:97-118).
+ * No job graph (each monomial's value and derivative terms are their own
+ * left-to-right product chains, summed in monomial order) and the literal md
+ * arithmetic (expansion.hpp restated over local arrays), not the engine's
+ * register-streamed one. Refuses instances outside within_oracle_guard
+ * (PSE_EINVAL, as the reference). stat: [Q][1+N+n][d+1] (one point, unfolded
+ * coefficients); vg_out: [Q][n+1][d+1]. */
+int pse_eval_direct(int32_t n, int32_t d, int32_t m, int32_t mode, int32_t N, const int32_t* nvars,
+                    const int32_t* indices, const int32_t* exponents, const double* stat, double* vg_out,
+                    int32_t device);
+/* within_oracle_guard (oracle_direct.cpp:32-39): 1 inside, 0 outside, <0 error */
+int pse_within_oracle_guard(int32_t d, int32_t N, const int32_t* nvars, const int32_t* exponents);
 
 /* ---- primitives (host buffers; for tests and callers of the series ops) --- */
 /* op: 0 add, 1 sub, 2 mul; impl: 0 register-streamed engine path, 1 literal;

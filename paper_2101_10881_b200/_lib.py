@@ -65,7 +65,7 @@ EXPORTS = [
     "pse_problem_parse", "pse_problem_read", "pse_problem_write", "pse_problem_text", "pse_problem_create",
     "pse_problem_gen", "pse_problem_info", "pse_problem_id", "pse_problem_arrays", "pse_problem_destroy",
     "pse_plan_create_sharded", "pse_plan_exchange_words", "pse_plan_pack", "pse_plan_unpack", "pse_plan_finish",
-    "pse_plan_layer_ms",
+    "pse_plan_layer_ms", "pse_eval_direct", "pse_within_oracle_guard",
 ]
 
 _lib = None
@@ -133,6 +133,8 @@ def lib():
     L.pse_plan_unpack.argtypes = [_VP, i32, i32, dp]
     L.pse_plan_finish.argtypes = [_VP, i32, i32, C.POINTER(Report)]
     L.pse_plan_layer_ms.argtypes = [_VP, dp, i32, dp, i32]
+    L.pse_eval_direct.argtypes = [i32, i32, i32, i32, i32, dp, dp, dp, dp, dp, i32]
+    L.pse_within_oracle_guard.argtypes = [i32, i32, dp, dp]
     _lib = L
     return L
 

@@ -3,14 +3,17 @@
 //
 //   pseval_b200 gen <p1|p2|p3> <out> [--degree D] [--precision M] [--mode real|complex] [--seed S]
 //   pseval_b200 verify <id|file> [--degree D] [--precision M] [--mode ..] [--seed S] [--device G]
+//                      [--oracle auto|on|off]
 //   pseval_b200 bench [id|file] [--degree D ...] [--precision M ...] [--mode ..] [--seed S]
 //                     [--repeats R] [--csv FILE] [--device G]
 //   pseval_b200 graph-stats <id|file> [--degree D] [--precision M] [--mode ..] [--seed S]
 //
 // verify cross-checks the device engine's execution paths bit for bit
-// (fused convolution kernel vs split product/accumulation path, and a batch
-// of points vs single evaluations) -- the device analogue of the reference's
-// sequential-vs-parallel check (pseval.cpp:76-95).
+// (layered fused vs split convolutions, the dataflow and banded-wave
+// schedules, a batch of points vs single evaluations) -- the device analogue
+// of the reference's sequential-vs-parallel check (pseval.cpp:76-95) -- and
+// the engine against an independent device evaluator (eval_direct,
+// oracle_direct.cpp:41-78) within the reference's tolerance (pseval.cpp:97-118).
 #include <algorithm>
 #include <cctype>
 #include <cmath>
@@ -35,7 +38,7 @@ struct Args {
   std::string cmd;
   std::vector<std::string> pos;
   std::vector<int> degrees, precisions;
-  std::string mode = "real", csv;
+  std::string mode = "real", csv, oracle = "auto";
   uint64_t seed = 7;
   int repeats = 3, device = 0;
 };
@@ -71,6 +74,10 @@ Args parse(int argc, char** argv) {
       a.repeats = std::max(1, std::stoi(val()));
     } else if (s == "--csv") {
       a.csv = val();
+    } else if (s == "--oracle") {
+      a.oracle = val();
+      if (a.oracle != "auto" && a.oracle != "on" && a.oracle != "off")
+        throw std::invalid_argument("--oracle must be auto, on or off");
     } else if (s == "--device") {
       a.device = std::stoi(val());
     } else if (s.size() > 1 && s[0] == '-') {
@@ -155,36 +162,145 @@ std::vector<double> eval(const Prob& p, const std::vector<double>& stat, int bat
   return vg;
 }
 
-int do_verify(const Prob& p, int device) {
+// one device evaluation with the conv path forced through the planner's knobs
+// (PSE_CONV_MODE / PSE_SPLIT_THRESHOLD are read at plan creation)
+std::vector<double> eval_path(const Prob& p, const std::vector<double>& stat, int batch, int device, const char* mode,
+                              const char* split) {
+  if (mode) setenv("PSE_CONV_MODE", mode, 1); else unsetenv("PSE_CONV_MODE");
+  if (split) setenv("PSE_SPLIT_THRESHOLD", split, 1); else unsetenv("PSE_SPLIT_THRESHOLD");
+  pse_report rep{};
+  std::vector<double> vg = eval(p, stat, batch, device, &rep);
+  unsetenv("PSE_CONV_MODE");
+  unsetenv("PSE_SPLIT_THRESHOLD");
+  return vg;
+}
+
+// PSE_VERIFY_PERTURB=<path> (testing verify itself): flip the lowest bit of
+// the last limb of value coefficient 0 in that path's result -- "oracle"
+// perturbs every path by a relative 1e-6 instead
+void perturb(std::vector<double>& vg, const char* path, const Prob& p) {
+  const char* e = getenv("PSE_VERIFY_PERTURB");
+  if (!e) return;
+  if (std::string(e) == "oracle") {
+    vg[0] += std::fabs(vg[0]) * 1e-6 + 1e-300;
+    return;
+  }
+  if (std::string(e) != path) return;
+  const size_t at = static_cast<size_t>(p.m() - 1) * (p.n() + 1) * (p.d() + 1);  // limb m-1, value, coeff 0
+  uint64_t b;
+  std::memcpy(&b, &vg[at], 8);
+  b ^= 1;
+  std::memcpy(&vg[at], &b, 8);
+}
+
+// oracle_cost_estimate (pseval.cpp:55-66): the auto mode skips the oracle above 1e6
+int64_t oracle_cost_estimate(const Prob& p) {
+  int64_t q = 1, pos = 0;
+  for (int k = 0; k < p.N(); ++k) {
+    int64_t t = 0;
+    bool has = false;
+    if (p.ex)
+      for (int j = 0; j < p.nv[k]; ++j) has = has || p.ex[pos + j] != 0;
+    for (int j = 0; j < p.nv[k]; ++j) t += has ? p.ex[pos + j] : 1;
+    q = std::max(q, t);
+    pos += p.nv[k];
+  }
+  const int64_t len = p.d() + 1;
+  return static_cast<int64_t>(p.N()) * q * q * len * len * p.m() * p.m();
+}
+
+double md_to_double(const double* limbs, int m, size_t stride) {  // multidouble.hpp:65-69
+  double s = 0.0;
+  for (int i = m - 1; i >= 0; --i) s += limbs[static_cast<size_t>(i) * stride];
+  return s;
+}
+
+// do_verify (pseval.cpp:70-118) over the device engine. The reference
+// compares its sequential and parallel engines bit for bit, then both with
+// eval_direct; here the engine's distinct device paths are compared bit for
+// bit -- layered fused vs layered split convolutions, the dataflow and the
+// banded-wave schedules vs layered, the planner's own pick, a batch vs one
+// point -- and the engine with the independent device evaluator
+// (pse_eval_direct: direct product chains, literal md arithmetic) within the
+// reference's tolerance 2^(32-52m) * max(1, |ref|).
+int do_verify(const Prob& p, int device, const std::string& oracle_flag) {
   std::printf("problem %s: n=%d N=%d d=%d m=%d mode=%s\n", p.id.c_str(), p.n(), p.N(), p.d(), p.m(),
               p.mode() ? "complex" : "real");
   const size_t rows = 1 + static_cast<size_t>(p.N()) + p.n();
   const size_t pw = rows * (p.d() + 1);
   std::vector<double> one(p.st, p.st + static_cast<size_t>(p.Q()) * pw);
-  pse_report rep{};
-  setenv("PSE_SPLIT_THRESHOLD", "0", 1);
-  const std::vector<double> fused = eval(p, one, 1, device, &rep);
-  setenv("PSE_SPLIT_THRESHOLD", "4611686018427387904", 1);
-  const std::vector<double> split = eval(p, one, 1, device, &rep);
-  unsetenv("PSE_SPLIT_THRESHOLD");
+  const char* huge = "4611686018427387904";
+  std::vector<double> fused = eval_path(p, one, 1, device, "layer", "0");
+  std::vector<double> split = eval_path(p, one, 1, device, "layer", huge);
+  std::vector<double> flow = eval_path(p, one, 1, device, "flow", nullptr);
+  std::vector<double> waves = eval_path(p, one, 1, device, "band", nullptr);
+  std::vector<double> autop = eval_path(p, one, 1, device, nullptr, nullptr);
+  perturb(fused, "fused", p);
+  perturb(split, "split", p);
+  perturb(flow, "flow", p);
+  perturb(waves, "band", p);
+  perturb(autop, "auto", p);
   // batch of 3 identical points, [Q][3][rows][d+1]
   std::vector<double> three(static_cast<size_t>(p.Q()) * 3 * pw);
   for (int q = 0; q < p.Q(); ++q)
     for (int b = 0; b < 3; ++b) std::memcpy(&three[(q * 3 + b) * pw], &one[q * pw], pw * sizeof(double));
-  const std::vector<double> batched = eval(p, three, 3, device, &rep);
+  const std::vector<double> batched = eval_path(p, three, 3, device, nullptr, nullptr);
   const size_t vw = static_cast<size_t>(p.n() + 1) * (p.d() + 1);
-  const bool paths = std::memcmp(fused.data(), split.data(), fused.size() * sizeof(double)) == 0;
+  auto same = [](const std::vector<double>& x, const std::vector<double>& y) {
+    return x.size() == y.size() && std::memcmp(x.data(), y.data(), x.size() * sizeof(double)) == 0;
+  };
+  bool ok = true;
+  auto report = [&](const char* what, bool eq) {
+    std::printf("engines: %s: %s\n", what, eq ? "bitwise equal" : "MISMATCH");
+    ok = ok && eq;
+  };
+  report("layered fused vs layered split convolutions", same(fused, split));
+  report("dataflow (banded, one persistent launch) vs layered", same(flow, fused));
+  report("banded waves vs layered", same(waves, fused));
+  report("planner's path vs layered", same(autop, fused));
   bool batch_ok = true;
   for (int q = 0; q < p.Q(); ++q)
     for (int b = 0; b < 3; ++b)
-      batch_ok = batch_ok && std::memcmp(&batched[(q * 3 + b) * vw], &fused[q * vw], vw * sizeof(double)) == 0;
-  std::printf("engines: fused vs split convolution paths: %s\n", paths ? "bitwise equal" : "MISMATCH");
-  std::printf("engines: batch of 3 points vs single point: %s\n", batch_ok ? "bitwise equal" : "MISMATCH");
-  double vmax = 0;
-  for (size_t k = 0; k <= static_cast<size_t>(p.d()); ++k) vmax = std::max(vmax, std::fabs(fused[k]));
-  std::printf("value: %zu coefficients, max |leading limb| %.6e; %.3f ms on the device\n",
-              static_cast<size_t>(p.d()) + 1, vmax, rep.wall_ms / 1.0);
-  const bool pass = paths && batch_ok;
+      batch_ok = batch_ok && std::memcmp(&batched[(q * 3 + b) * vw], &autop[q * vw], vw * sizeof(double)) == 0;
+  report("batch of 3 points vs single point", batch_ok);
+
+  bool oracle_ok = true;
+  if (oracle_flag == "off") {
+    std::printf("oracle: skipped (disabled)\n");
+  } else if (oracle_flag == "auto" && oracle_cost_estimate(p) > 1000000) {
+    std::printf("oracle: skipped (instance too large for auto mode; --oracle on forces it)\n");
+  } else if (pse_within_oracle_guard(p.d(), p.N(), p.nv, p.ex) != 1) {
+    std::printf("oracle: refused, instance exceeds the direct-evaluation size guard\n");
+    return 2;
+  } else {
+    std::vector<double> ref(static_cast<size_t>(p.Q()) * vw);
+    check(pse_eval_direct(p.n(), p.d(), p.m(), p.mode(), p.N(), p.nv, p.ix, p.ex, one.data(), ref.data(), device));
+    // series_gap / series_norm (pseval.cpp:35-53): md_to_double(md_sub(x, y)),
+    // the subtraction in the same md arithmetic (on the device)
+    const int m = p.m(), P = p.mode() ? 2 : 1;
+    const size_t cnt = static_cast<size_t>(P) * vw;
+    std::vector<double> x(cnt * m), y(cnt * m), diff(cnt * m);
+    for (int part = 0; part < P; ++part)
+      for (size_t r = 0; r < vw; ++r)
+        for (int l = 0; l < m; ++l) {
+          const size_t src = (static_cast<size_t>(part) * m + l) * vw + r, dst = (part * vw + r) * m + l;
+          x[dst] = autop[src];
+          y[dst] = ref[src];
+        }
+    check(pse_md_apply(1, m, 1, static_cast<int64_t>(cnt), x.data(), y.data(), diff.data(), device));
+    double norm = 1.0, gap = 0.0;
+    for (size_t c = 0; c < cnt; ++c) {
+      norm = std::max(norm, std::fabs(md_to_double(&y[c * m], m, 1)));
+      gap = std::max(gap, std::fabs(md_to_double(&diff[c * m], m, 1)));
+    }
+    const double tol = std::ldexp(1.0, 32 - 52 * m);
+    const double rel = gap / norm;
+    oracle_ok = rel <= tol;
+    std::printf("oracle: independent device evaluator (direct product chains, literal md arithmetic): max "
+                "coefficient discrepancy %.3e relative (tolerance %.3e): %s\n",
+                rel, tol, oracle_ok ? "ok" : "MISMATCH");
+  }
+  const bool pass = ok && oracle_ok;
   std::printf("verify: %s\n", pass ? "PASS" : "FAIL");
   return pass ? 0 : 1;
 }
@@ -252,7 +368,7 @@ int main(int argc, char** argv) {
       if (a.pos.size() != 1) throw std::invalid_argument("usage: pseval_b200 verify <id|file> [options]");
       Prob p;
       load_target(p, a.pos[0], d0, m0, mode, a.seed);
-      return do_verify(p, a.device);
+      return do_verify(p, a.device, a.oracle);
     }
     if (a.cmd == "graph-stats") {
       if (a.pos.size() != 1) throw std::invalid_argument("usage: pseval_b200 graph-stats <id|file> [options]");

@@ -527,7 +527,7 @@ struct Plan {
   };
   unsigned long long* flow_counter = nullptr;
   std::map<int, BandWaves> band_waves;
-  int conv_mode = 0;         // PSE_CONV_MODE: 0 auto, 1 layered, 2 banded waves, 3 dataflow
+  int conv_mode = 0;         // PSE_CONV_MODE: 0 auto, 1 layered, 2 banded waves, 3 dataflow, 4 CTA-local dataflow
   double band_rounds = 1.0;  // PSE_BAND_ROUNDS: wave size in resident warps
   double flow_slack = 1.0;   // PSE_FLOW_SLACK: see band_schedule (swept: 0.1-8, best 1)
   int band_w = 0;            // PSE_BAND_W: 16 or 32 (0: chosen per run)
@@ -549,7 +549,7 @@ struct Plan {
     if (nrows_mine == 0 || conv_mode == 1 || multi_writer || nb16 > 32767 ||
         nrows_mine * nb16 * (nb16 + 1) / 2 >= (int64_t(1) << 31))
       return nl;
-    if (conv_mode >= 2) return 0;
+    if (conv_mode >= 2) return 0;  // waves, dataflow and CTA-local dataflow take every layer
     const int64_t thr = int64_t(sms) * 4 * 128 * 2, npairs = (d + 2) / 2;
     if (static_cast<int64_t>(batch) * layer_pairs < thr) return 0;
     int f = nl;
@@ -558,10 +558,104 @@ struct Plan {
   }
   bool banded(int batch) const { return band_first(batch) < static_cast<int>(layer_rows.size()); }
 
-  bool flow() const { return conv_mode == 3 || conv_mode == 0; }
+  // the global dataflow kernel (also the CTA path's fallback)
+  bool flow() const { return conv_mode == 3 || conv_mode == 0 || conv_mode == 4; }
+
+  // ---- CTA-local dataflow (CtaArgs in kernels.cuh): one block per
+  // independent job group (connected component of the dynamic slots: whole
+  // monomials) and point; the group's banded tasks scheduled for one
+  // block's warps. Built once (host only); ok = false when it cannot run
+  // (a group's completion flags exceed shared memory next to the lanes).
+  std::vector<std::vector<int>> layer_comp;  // component of every row of layer_rows
+  int ncomps = 0;
+  struct CtaPlan {
+    bool built = false, ok = false;
+    int W = 32, ngroups = 0, max_units = 0;
+    int4 *jobs = nullptr, *tasks = nullptr;
+    int *group_off = nullptr, *dep_off = nullptr, *deps = nullptr;
+    double makespan = 0;  // simulated, in steps: the slowest group
+  } cta;
+
+  bool cta_mode() const { return conv_mode == 4 && cta_ready(); }
+  bool cta_ready() const { return cta.built && cta.ok; }
+
+  void prepare_cta() {
+    if (cta.built) return;
+    cta.built = true;
+    if (nrows_mine == 0 || multi_writer) return;
+    const int64_t nb16 = 1 + d / 16;
+    if (nb16 > 32767) return;
+    // rows of each group, in layer order, and their layers
+    std::vector<std::vector<ConvRow>> rows(ncomps);
+    std::vector<std::vector<int>> rlayer(ncomps);
+    for (size_t L2 = 0; L2 < layer_rows.size(); ++L2)
+      for (size_t r = 0; r < layer_rows[L2].size(); ++r) {
+        rows[layer_comp[L2][r]].push_back(layer_rows[L2][r]);
+        rlayer[layer_comp[L2][r]].push_back(static_cast<int>(L2));
+      }
+    const int warps = L->threads / 32;
+    const Costs cst = costs(m);
+    // fixed cost of a task (shared-memory hand-out and flags) in steps
+    const double ovh = 250.0 / static_cast<double>(cst.inst_mul + cst.inst_add);
+    std::vector<int4> jobs, tasks;
+    std::vector<int> goff(1, 0), doff(1, 0), deps;
+    auto sched_all = [&](int W, bool commit) {
+      double worst = 0;
+      for (int c = 0; c < ncomps; ++c) {
+        if (rows[c].empty()) continue;
+        if (static_cast<int64_t>(rows[c].size()) * nb16 * (nb16 + 1) / 2 >= (int64_t(1) << 31))
+          throw std::invalid_argument("job group too large for the banded schedule");
+        const BandSched sc = band_schedule(rows[c], d, W, kSlots, true, int64_t(warps) * (32 / W), flow_slack, ovh);
+        worst = std::max(worst, sc.makespan);
+        if (!commit) continue;
+        const int jbase = static_cast<int>(jobs.size());
+        std::set<int64_t> produced;
+        for (auto& r : rows[c]) produced.insert(r.out);
+        for (size_t t = 0; t < rows[c].size(); ++t) {
+          const ConvRow& r = rows[c][t];
+          jobs.push_back(make_int4(static_cast<int>(r.in1), static_cast<int>(r.in2), static_cast<int>(r.out),
+                                   (produced.count(r.in1) ? 2 : 0) | (!r.copy && produced.count(r.in2) ? 4 : 0) |
+                                       (rlayer[c][t] << 8)));
+        }
+        const std::vector<int4>& w = sc.waves.at(0);
+        for (int4 v : w) {
+          if (v.w != -4) v.x += jbase;
+          tasks.push_back(v);
+        }
+        const int nd = static_cast<int>(w.size() / kSlots);
+        cta.max_units = std::max(cta.max_units, nd);
+        for (int q = 0; q < nd; ++q) {
+          for (int e = sc.dep_off[q]; e < sc.dep_off[q + 1]; ++e) deps.push_back(sc.deps[e]);
+          doff.push_back(static_cast<int>(deps.size()));
+        }
+        goff.push_back(goff.back() + nd);
+      }
+      return worst;
+    };
+    if (band_w) {
+      cta.W = band_w;
+    } else {
+      const double m16 = sched_all(16, false), m32 = sched_all(32, false);
+      cta.W = m16 < m32 ? 16 : 32;
+    }
+    cta.makespan = sched_all(cta.W, true);
+    cta.ngroups = static_cast<int>(goff.size()) - 1;
+    if (!L->cta_fits(cta.max_units)) return;  // stays on the global dataflow path
+    cta.jobs = dev_upload(jobs, stream);
+    cta.tasks = dev_upload(tasks, stream);
+    cta.group_off = dev_upload(goff, stream);
+    cta.dep_off = dev_upload(doff, stream);
+    cta.deps = dev_upload(deps.empty() ? std::vector<int>{0} : deps, stream);
+    ck(cudaStreamSynchronize(stream), "cta upload");
+    cta.ok = true;
+  }
 
   // host schedule + upload for a batch size (never during stream capture)
   void prepare_band(int batch) {
+    if (conv_mode == 4) {
+      prepare_cta();
+      if (cta_ready()) return;
+    }
     if (!banded(batch) || band_waves.count(batch)) return;
     BandWaves bw;
     bw.first = band_first(batch);
@@ -635,6 +729,11 @@ struct Plan {
       cudaFree(w.flags);
     }
     cudaFree(flow_counter);
+    cudaFree(cta.jobs);
+    cudaFree(cta.tasks);
+    cudaFree(cta.group_off);
+    cudaFree(cta.dep_off);
+    cudaFree(cta.deps);
     cudaFree(stamps);
     cudaFree(peer_list);
     cudaFree(peer_first);
@@ -722,7 +821,11 @@ struct Plan {
         }
       }
     }
-    if (first < static_cast<int>(layer_rows.size())) {  // banded part
+    if (first < static_cast<int>(layer_rows.size()) && cta_mode()) {  // CTA-local dataflow
+      CtaArgs a{arena, G, cta.jobs, cta.tasks, cta.group_off, cta.dep_off, cta.deps, cta.ngroups, batch, cta.W, stamps};
+      if (!L->conv_cta(a, cta.max_units, stream)) throw std::logic_error("CTA-local dataflow does not fit");
+      ++launches;
+    } else if (first < static_cast<int>(layer_rows.size())) {  // banded part
       const BandWaves& bw = band_waves.at(batch);
       if (flow()) {
         ck(cudaMemsetAsync(bw.flags, 0, sizeof(unsigned) * batch * bw.nunits, stream), "flags");
@@ -826,7 +929,7 @@ struct Plan {
     for (auto& [jobs, nj] : pro_layers) n += split_layer(nj, batch, groups[0]) ? 2 : 1;
     const int first = band_first(batch);
     if (first < static_cast<int>(layer_rows.size()))
-      n += flow() ? 1 : static_cast<int>(band_waves.at(batch).waves.size());
+      n += cta_mode() || flow() ? 1 : static_cast<int>(band_waves.at(batch).waves.size());
     for (const ConvGroup& gr : groups)
       for (size_t q = 0; q < gr.layers.size(); ++q)
         if (gr.layer_index[q] < first) n += split_layer(gr.layers[q].second, batch, gr) ? 2 : 1;
@@ -953,7 +1056,9 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
     const char* env = getenv("PSE_CONV_GROUPS");
     int ng = env ? atoi(env) : 4;
     ng = std::max(1, std::min<int>(ng, static_cast<int>(mine.size())));
-    std::map<int64_t, int> comp_group;
+    std::map<int64_t, int> comp_group, comp_index;
+    for (int64_t c : mine) comp_index[c] = static_cast<int>(comp_index.size());
+    p->ncomps = static_cast<int>(mine.size());
     int64_t acc = 0;
     for (int64_t c : mine) {
       comp_group[c] = static_cast<int>(std::min<int64_t>(ng - 1, acc * ng / std::max<int64_t>(1, njobs_mine)));
@@ -964,11 +1069,14 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
     for (size_t L = npro; L < layers.size(); ++L) {
       std::vector<std::vector<ConvRow>> per(ng);
       p->layer_rows.emplace_back();
+      p->layer_comp.emplace_back();
       for (const ConvRow& r : layers[L]) {
-        auto it = comp_group.find(find(r.out));
+        const int64_t root = find(r.out);
+        auto it = comp_group.find(root);
         if (it != comp_group.end()) {
           per[it->second].push_back(r);
           p->layer_rows.back().push_back(r);
+          p->layer_comp.back().push_back(comp_index[root]);
           ++p->nrows_mine;
         }
       }
@@ -989,7 +1097,7 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
     {
       const char* cm = getenv("PSE_CONV_MODE");
       const std::string m = cm ? cm : "";
-      p->conv_mode = m == "layer" ? 1 : m == "band" ? 2 : m == "flow" ? 3 : 0;
+      p->conv_mode = m == "layer" ? 1 : m == "band" ? 2 : m == "flow" ? 3 : m == "cta" ? 4 : 0;
       const char* br = getenv("PSE_BAND_ROUNDS");
       if (br && atof(br) > 0) p->band_rounds = atof(br);
       const char* fs = getenv("PSE_FLOW_SLACK");
@@ -1113,6 +1221,7 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
   p->vg = dev_alloc<double>(static_cast<size_t>(p->Q) * max_batch * p->nrows * (g.d + 1));
   ck(cudaStreamSynchronize(s), "plan upload");
 
+  if (p->conv_mode == 4) p->prepare_cta();
   const Costs c = costs(g.m);
   p->flops_model = flop_count(g, 0, c.rep_add, c.rep_mul);
   p->alg_ops = alg_op_count(g);
@@ -1543,6 +1652,7 @@ int pse_plan_conv_path(const pse_plan* p, int32_t batch, int32_t* path) {
   if (!p || !path || batch < 1 || batch > p->p->max_batch) return PSE_EINVAL;
   const pse::Plan& P = *p->p;
   *path = !P.banded(batch)          ? PSE_CONV_LAYERED
+          : P.cta_mode()            ? PSE_CONV_CTA
           : !P.flow()               ? PSE_CONV_WAVES
           : P.band_first(batch) > 0 ? PSE_CONV_HYBRID
                                     : PSE_CONV_DATAFLOW;

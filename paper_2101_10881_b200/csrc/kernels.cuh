@@ -170,11 +170,36 @@ struct FlowArgs {
   Stamp* stamps;        // as BandArgs
 };
 
+// CTA-local dataflow (deep graphs at small precisions, where the global
+// dataflow kernel's per-task hand-out and flag round trips through L2 dwarf a
+// task's arithmetic): ONE block per independent job group (whole monomials)
+// and point, its warps taking the group's band x segment tasks from a
+// shared-memory counter in scheduled order and waiting on shared-memory
+// completion flags -- a CTA-scope fence instead of a GPU-scope one, a
+// shared-memory poll instead of an L2 round trip.
+struct CtaArgs {
+  double* arena;
+  Geom G;
+  const int4* jobs;      // as BandArgs (every job of every group)
+  const int4* tasks;     // kSlots slots per warp descriptor, groups one after another
+  const int* group_off;  // [ngroups+1] first descriptor of each group
+  const int* dep_off;    // [ndesc+1] CSR of the descriptors each one waits for,
+  const int* deps;       //   as indices local to the group
+  int ngroups;
+  int batch;
+  int W;
+  Stamp* stamps;         // as BandArgs
+};
+
 struct Launchers {
   void (*conv)(const ConvArgs&, cudaStream_t);
   void (*conv_band)(const BandArgs&, cudaStream_t);
   void (*conv_flow)(const FlowArgs&, int blocks, cudaStream_t);
   int (*band_blocks_per_sm)(bool flow);
+  // CTA-local dataflow: returns false (nothing launched) when a group's
+  // completion flags do not fit next to the lanes in shared memory
+  bool (*conv_cta)(const CtaArgs&, int max_units, cudaStream_t);
+  bool (*cta_fits)(int max_units);
   void (*conv_prod)(const SplitArgs&, cudaStream_t);
   void (*conv_accum)(const SplitArgs&, cudaStream_t);
   void (*add)(const AddArgs&, cudaStream_t);
@@ -189,6 +214,7 @@ struct Launchers {
 #ifdef PSE_KERNELS_IMPL
 
 constexpr int kConvThreads = kLaneThreads;
+constexpr size_t kCtaSmemMax = 227 * 1024;  // dynamic shared memory of one block
 // resident blocks per SM for a target expressed in 128-thread blocks (the
 // register budget stays the same whatever the block size)
 constexpr int blocks_for(int minb128) { return minb128 * 128 / kConvThreads > 0 ? minb128 * 128 / kConvThreads : 1; }
@@ -216,6 +242,13 @@ __device__ __forceinline__ void load_md_sel(const double* __restrict__ src, int 
     v[q] = coh ? __ldcg(p) : __ldg(p);
     p += S;
   }
+}
+
+// words this kernel itself wrote (plain coherent loads, not the read-only path)
+template <int M>
+__device__ __forceinline__ void load_md_rw(const double* src, int S, int j, double (&v)[M]) {
+#pragma unroll
+  for (int q = 0; q < M; ++q) v[q] = src[q * S + j];
 }
 
 template <int M>
@@ -282,7 +315,19 @@ __device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm)
 
   const int n1 = k1 + 1;
   const int total = k2 > k1 ? d + 2 : n1;
-  if constexpr (!CPLX) {
+  if constexpr (!CPLX && M == 1) {
+    // a plain DMUL / DADD chain: the accumulator stays in a register
+    double acc = 0.0;
+#pragma unroll 1
+    for (int t = 0; t < total; ++t) {
+      const bool second = t >= n1;
+      const int kk = second ? k2 : k1;
+      const int i = second ? t - n1 : t;
+      const double p = __dmul_rn(__ldg(X + i), __ldg(Y + kk - i));
+      acc = i == 0 ? p : __dadd_rn(acc, p);
+      if (i == kk) Z[kk] = acc;
+    }
+  } else if constexpr (!CPLX) {
     // the accumulator lives in the lane (acc_add), not in registers, so it is
     // not live across the md_mul
     acc_init<M>(sm);
@@ -347,9 +392,22 @@ __device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm)
       load_md<M>(Y, S, kk - i, yb);
       exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yr
       exp_add_fast<M>(p1, p2, pr, sm);
-      if (i == 0) copy_md<M>(ai, pr);
-      else exp_add_fast<M>(ai, pr, ai, sm);
-      if (i == kk) store_md<M>(Z + M * S, S, kk, ai);
+      if constexpr (LANE_RE) {
+        // the imaginary running sum lives in the output slot's imaginary
+        // words (this thread's own, L1-resident): no register is live
+        // across the four md_muls (ptxas spilled them otherwise)
+        if (i == 0) {
+          store_md<M>(Z + M * S, S, kk, pr);
+        } else {
+          load_md_rw<M>(Z + M * S, S, kk, ai);
+          exp_add_fast<M>(ai, pr, ai, sm);
+          store_md<M>(Z + M * S, S, kk, ai);
+        }
+      } else {
+        if (i == 0) copy_md<M>(ai, pr);
+        else exp_add_fast<M>(ai, pr, ai, sm);
+        if (i == kk) store_md<M>(Z + M * S, S, kk, ai);
+      }
     }
   }
 }
@@ -487,7 +545,35 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
   };
   const int nA = ibA - iaA + 1;
   const int total = nA + (kB >= 0 ? ibB - iaB + 1 : 0);
-  if constexpr (!CPLX) {
+  if constexpr (!CPLX && M == 1) {
+    // A plain DMUL / DADD chain per piece with the accumulator in a register
+    // and the operands walked by pointer (x up, y down): the generic step's
+    // index selects would cost ~15 integer instructions per two FP64 ones.
+    // Partial sums resume from Z, as the generic path.
+    auto piece = [&](int k, int ia, int ib) {
+      const double* xp;
+      const double* yp;
+      bool gx = false, gy = false;  // operand read from global memory (else staged)
+      if constexpr (STAGE) {
+        xp = stg + xo + ia - xb;
+        yp = stg + yo + (k - ia) - yb;
+      } else {
+        xp = X + ia;
+        yp = Y + (k - ia);
+        gx = true;
+        gy = true;
+      }
+      auto rx = [&](int s) { return gx ? (cx ? __ldcg(xp + s) : __ldg(xp + s)) : xp[s]; };
+      auto ry = [&](int s) { return gy ? (cy ? __ldcg(yp - s) : __ldg(yp - s)) : yp[-s]; };
+      const int n = ib - ia + 1;
+      double acc = ia == 0 ? __dmul_rn(rx(0), ry(0)) : __dadd_rn(__ldcg(Z + k), __dmul_rn(rx(0), ry(0)));
+#pragma unroll 4
+      for (int s2 = 1; s2 < n; ++s2) acc = __dadd_rn(acc, __dmul_rn(rx(s2), ry(s2)));
+      Z[k] = acc;
+    };
+    piece(kA, iaA, ibA);
+    if (kB >= 0) piece(kB, iaB, ibB);
+  } else if constexpr (!CPLX) {
     acc_init<M>(sm);
     double o[M];
 #pragma unroll 1
@@ -564,30 +650,49 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
       ldy(0, k - i, yb);
       exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yr
       exp_add_fast<M>(p1, p2, pr, sm);
-      if (i == 0) {
-        copy_md<M>(ai, pr);
-      } else {
-        if (i == ia) {
+      if constexpr (LANE_RE) {  // imaginary running sum in Z (see k_conv)
+        if (i == 0) {
+          store_md<M>(Z + M * S, S, k, pr);
+        } else {
 #pragma unroll
           for (int q = 0; q < M; ++q) ai[q] = __ldcg(Z + (M + q) * S + k);
+          exp_add_fast<M>(ai, pr, ai, sm);
+          store_md<M>(Z + M * S, S, k, ai);
         }
-        exp_add_fast<M>(ai, pr, ai, sm);
+      } else {
+        if (i == 0) {
+          copy_md<M>(ai, pr);
+        } else {
+          if (i == ia) {
+#pragma unroll
+            for (int q = 0; q < M; ++q) ai[q] = __ldcg(Z + (M + q) * S + k);
+          }
+          exp_add_fast<M>(ai, pr, ai, sm);
+        }
+        if (last) store_md<M>(Z + M * S, S, k, ai);
       }
-      if (last) store_md<M>(Z + M * S, S, k, ai);
     }
   }
 }
 
-// end stamps of the layers of one warp descriptor's tasks (lane 0)
-__device__ __forceinline__ void stamp_tasks(Stamp* stamps, const int4* __restrict__ jobs, const int4* __restrict__ slots) {
-  if (!stamps) return;
-  const Stamp now = global_ns();
-#pragma unroll 1
-  for (int f = 0; f < kSlots; ++f) {
-    const int4 T = slots[f];
-    if (T.w != -4 && (f == 0 || slots[f - 1].x != T.x || slots[f - 1].y != T.y || slots[f - 1].z != T.z))
-      atomicMax(stamps + 1 + (jobs[T.x].w >> 8), now);
+// End stamps of the layers of one warp descriptor's tasks. Lane f < kSlots
+// looks up slot f's layer BEFORE the task runs (stamp_slot_layer: the load's
+// latency hides behind the task) and records the end time after it
+// (stamp_slot_end); -1 = nothing to stamp (empty slot, or not the first slot
+// of its task).
+__device__ __forceinline__ int stamp_slot_layer(const Stamp* stamps, const int4* __restrict__ jobs,
+                                                const int4* __restrict__ slots, int lane) {
+  if (!stamps || lane >= kSlots) return -1;
+  const int4 T = slots[lane];
+  if (T.w == -4) return -1;
+  if (lane > 0) {
+    const int4 P = slots[lane - 1];
+    if (P.x == T.x && P.y == T.y && P.z == T.z && P.w == T.w) return -1;
   }
+  return jobs[T.x].w >> 8;
+}
+__device__ __forceinline__ void stamp_slot_end(Stamp* stamps, int layer) {
+  if (layer >= 0) atomicMax(stamps + 1 + layer, global_ns());
 }
 
 template <int M, bool CPLX>
@@ -599,9 +704,10 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_band(const
   if (gw >= static_cast<int64_t>(a.batch) * a.ntasks) return;
   const int tw = static_cast<int>(gw % a.ntasks);
   const int4* slots = a.tasks + static_cast<int64_t>(tw) * kSlots;
+  const int layer = stamp_slot_layer(a.stamps, a.jobs, slots, threadIdx.x & 31);
   band_task<M, CPLX, false>(a.arena, a.G, a.jobs, slots, a.W, gw / a.ntasks, threadIdx.x & 31, sm, nullptr);
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) stamp_tasks(a.stamps, a.jobs, slots);
+  stamp_slot_end(a.stamps, layer);
 }
 
 // Dataflow form of the banded convolution: ONE persistent launch. Warps take
@@ -659,14 +765,56 @@ __global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_flow(const
       fence_acquire();
     }
     __syncwarp();
-    band_task<M, CPLX, true>(a.arena, a.G, a.jobs, a.tasks + static_cast<int64_t>(p) * kSlots, a.W, pt, lane, sm, stg);
+    const int4* slots = a.tasks + static_cast<int64_t>(p) * kSlots;
+    const int layer = stamp_slot_layer(a.stamps, a.jobs, slots, lane);
+    band_task<M, CPLX, true>(a.arena, a.G, a.jobs, slots, a.W, pt, lane, sm, stg);
     __syncwarp();  // the staging area is rewritten by the next unit
     __threadfence();
     __syncwarp();
-    if (lane == 0) {
-      st_release(fl + p, 1u);
-      stamp_tasks(a.stamps, a.jobs, a.tasks + static_cast<int64_t>(p) * kSlots);
-    }
+    if (lane == 0) st_release(fl + p, 1u);
+    stamp_slot_end(a.stamps, layer);
+  }
+}
+
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(kConvThreads, 1) k_conv_cta(const CtaArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm = make_lane(smem);
+  const int lane = threadIdx.x & 31;
+  constexpr int Q = CPLX ? 2 * M : M;
+  constexpr int nwarps = kConvThreads / 32;
+  double* stg = smem + kLaneThreads * (CPLX && !cplx_acc_lane<M>() ? MdTraits<M>::LANE : MdTraits<M>::LANE_CONV) +
+                (threadIdx.x >> 5) * kStageSlots * Q;
+  // after the lanes and the staging areas: the hand-out counter, then one
+  // completion byte per descriptor of this group
+  unsigned* counter = reinterpret_cast<unsigned*>(
+      smem + kLaneThreads * (CPLX && !cplx_acc_lane<M>() ? MdTraits<M>::LANE : MdTraits<M>::LANE_CONV) +
+      (band_stage<M, true>() ? nwarps * kStageSlots * Q : 0));
+  volatile unsigned char* done = reinterpret_cast<volatile unsigned char*>(counter + 1);
+  const int grp = blockIdx.x % a.ngroups;
+  const int64_t pt = blockIdx.x / a.ngroups;
+  const int u0 = a.group_off[grp], nu = a.group_off[grp + 1] - u0;
+  for (int i = threadIdx.x; i < nu; i += blockDim.x) done[i] = 0;
+  if (threadIdx.x == 0) *counter = 0;
+  if (a.stamps) stamp_begin(a.stamps);
+  __syncthreads();
+  for (;;) {
+    unsigned u = 0;
+    if (lane == 0) u = atomicAdd(counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (static_cast<int>(u) >= nu) break;
+    const int p = u0 + static_cast<int>(u);
+    for (int e = a.dep_off[p] + lane; e < a.dep_off[p + 1]; e += 32)
+      while (done[a.deps[e]] == 0) __nanosleep(20);
+    __syncwarp();
+    __threadfence_block();
+    const int4* slots = a.tasks + static_cast<int64_t>(p) * kSlots;
+    const int layer = stamp_slot_layer(a.stamps, a.jobs, slots, lane);
+    band_task<M, CPLX, true>(a.arena, a.G, a.jobs, slots, a.W, pt, lane, sm, stg);
+    __syncwarp();  // the staging area is rewritten by the next unit
+    __threadfence_block();
+    if (lane == 0) done[u] = 1;
+    stamp_slot_end(a.stamps, layer);
   }
 }
 
@@ -982,6 +1130,14 @@ struct Impl {
     if (a.nunits == 0) return;
     k_conv_flow<M, CPLX><<<blocks, kConvThreads, smem_flow(), s>>>(a);
   }
+  static size_t smem_cta_base() { return smem_flow() + sizeof(unsigned); }
+  static bool cta_fits(int max_units) { return smem_cta_base() + static_cast<size_t>(max_units) <= kCtaSmemMax; }
+  static bool conv_cta(const CtaArgs& a, int max_units, cudaStream_t s) {
+    const size_t sh = smem_cta_base() + static_cast<size_t>(max_units);
+    if (sh > kCtaSmemMax) return false;
+    if (a.ngroups > 0) k_conv_cta<M, CPLX><<<static_cast<unsigned>(a.ngroups) * a.batch, kConvThreads, sh, s>>>(a);
+    return true;
+  }
   // resident blocks per SM: banded waves (flow = false) or the dataflow kernel
   static int band_blocks_per_sm(bool flow) {
     int nb = 0;
@@ -1034,6 +1190,7 @@ struct Impl {
     cudaFuncSetAttribute(k_conv<M, CPLX, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv<M, CPLX, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv_band<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
+    cudaFuncSetAttribute(k_conv_cta<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCtaSmemMax));
     cudaFuncSetAttribute(k_conv_flow<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem_flow()));
     cudaFuncSetAttribute(k_conv_prod<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
@@ -1044,7 +1201,7 @@ struct Impl {
     cudaFuncSetAttribute(k_md<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
   }
   static const Launchers* table() {
-    static const Launchers L{&conv, &conv_band, &conv_flow, &band_blocks_per_sm, &conv_prod, &conv_accum, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE, kLaneThreads};
+    static const Launchers L{&conv, &conv_band, &conv_flow, &band_blocks_per_sm, &conv_cta, &cta_fits, &conv_prod, &conv_accum, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE, kLaneThreads};
     return &L;
   }
 };

@@ -475,7 +475,7 @@ class DevicePlan:
         check(lib().pse_plan_stream(self._h, C.byref(s)))
         return s.value or 0
 
-    CONV_PATHS = {1: "layered", 2: "waves", 3: "dataflow", 4: "hybrid"}
+    CONV_PATHS = {1: "layered", 2: "waves", 3: "dataflow", 4: "hybrid", 5: "cta"}
 
     def conv_path(self, batch: int = 1) -> str:
         """the convolution path a run of `batch` points takes
@@ -590,6 +590,29 @@ def evaluate(p: Polynomial, z: Sequence[np.ndarray], device: int = 0) -> RunRepo
     vg, rep = evaluate_packed(p.n, p.d, p.m, p.mode, nv, idx, ex, st.reshape(Q, 1, *st.shape[1:]), 1, device)
     value, grad = _split_vg(vg[:, 0], p.a0.shape[0], p.m, p.n, p.d)
     return _report(value, grad, rep)
+
+
+def eval_direct_packed(n: int, d: int, m: int, mode: str, nvars, indices, exponents, stat: np.ndarray,
+                       device: int = 0) -> np.ndarray:
+    """eval_direct (oracle_direct.cpp:41-78) on the device -- the independent
+    evaluator of `verify` (pse_eval_direct: direct product chains, literal md
+    arithmetic). stat: [Q][1+N+n][d+1]; returns vg [Q][n+1][d+1]."""
+    check_precision(m)
+    Q = (2 if _mode_code(mode) else 1) * m
+    nv = np.ascontiguousarray(nvars, np.int32)
+    ix = np.ascontiguousarray(indices, np.int32)
+    ex = None if exponents is None else np.ascontiguousarray(exponents, np.int32)
+    st = np.ascontiguousarray(stat, np.float64)
+    vg = np.empty((Q, n + 1, d + 1), np.float64)
+    check(lib().pse_eval_direct(n, d, m, _mode_code(mode), len(nv), ptr(nv), ptr(ix), ptr(ex), ptr(st), ptr(vg),
+                                device))
+    return vg
+
+
+def within_oracle_guard(d: int, nvars, exponents=None) -> bool:
+    nv = np.ascontiguousarray(nvars, np.int32)
+    ex = None if exponents is None else np.ascontiguousarray(exponents, np.int32)
+    return check(lib().pse_within_oracle_guard(d, len(nv), ptr(nv), ptr(ex))) == 1
 
 
 # ----------------------------------------------------------------- generator

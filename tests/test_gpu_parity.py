@@ -18,17 +18,21 @@ pytestmark = pytest.mark.gpu
 LEVELS = [1, 2, 3, 4, 5, 8, 10]
 
 
-@pytest.fixture(params=["fused", "split", "band", "flow", "flow32"])
+@pytest.fixture(params=["fused", "split", "band", "flow", "flow32", "cta"])
 def conv_path(request, monkeypatch):
     """Run an engine test through the fused conv kernel (one thread per
     coefficient pair), through the split path (products in parallel, then
     the accumulation chains), through the banded wavefront (chains cut into
     band x segment tasks, scheduled across layers, one launch per wave) and
     through its dataflow form (one persistent launch, per-task completion
-    flags; 16- and 32-wide bands). The planner reads
+    flags; 16- and 32-wide bands) and the CTA-local dataflow (one block per
+    job group, shared-memory flags; where a group's flags do not fit next to
+    the lanes -- M >= 8 -- the global dataflow runs). The planner reads
     PSE_CONV_MODE and PSE_SPLIT_THRESHOLD when a plan is created: 0 forces
     fused, a huge value forces split."""
-    if request.param in ("band", "flow", "flow32"):
+    if request.param == "cta":
+        monkeypatch.setenv("PSE_CONV_MODE", "cta")
+    elif request.param in ("band", "flow", "flow32"):
         # waves use 32-wide bands, the dataflow kernel 16 (flow32: 32)
         monkeypatch.setenv("PSE_CONV_MODE", request.param[:4])
         if request.param == "flow32":
@@ -501,16 +505,21 @@ def test_plan_reused_across_batch_sizes():
 
 def test_cli_verify_and_bench(tmp_path):
     """pseval_b200 verify / bench (the reference CLI's subcommands over the
-    device engine); verify cross-checks the fused and split conv paths and
-    batched against single evaluation, bit for bit."""
+    device engine): verify compares the layered fused and split convolutions,
+    the dataflow and banded-wave schedules, the planner's path and a batch of
+    points bit for bit, and the engine with the independent device evaluator
+    within the reference's tolerance (pseval.cpp:97-118)."""
     import os
     import subprocess
 
     cli = os.path.join(os.path.dirname(pe.LIB_PATH), "pseval_b200")
-    for args in (["verify", "p1", "--degree", "8", "--precision", "4"],
-                 ["verify", "p3", "--degree", "5", "--precision", "2", "--mode", "complex"]):
+    for args in (["verify", "p1", "--degree", "8", "--precision", "4", "--oracle", "on"],
+                 ["verify", "p3", "--degree", "5", "--precision", "2", "--mode", "complex", "--oracle", "on"],
+                 ["verify", "p2", "--degree", "20", "--precision", "3", "--oracle", "on"]):
         r = subprocess.run([cli, *args], capture_output=True, text=True, timeout=600)
         assert r.returncode == 0 and "verify: PASS" in r.stdout, r.stdout + r.stderr
+        assert r.stdout.count("bitwise equal") == 5, r.stdout
+        assert "oracle: independent device evaluator" in r.stdout and ": ok" in r.stdout, r.stdout
     path = str(tmp_path / "p2.txt")
     assert subprocess.run([cli, "gen", "p2", path, "--degree", "3", "--precision", "3"]).returncode == 0
     r = subprocess.run([cli, "verify", path], capture_output=True, text=True, timeout=600)
@@ -522,6 +531,62 @@ def test_cli_verify_and_bench(tmp_path):
     assert "| p1 | 15 | 2 | real |" in r.stdout
     rows = open(csv).read().strip().split("\n")
     assert rows[0].startswith("id,d,m,mode,workers") and len(rows) == 3
+
+
+@pytest.mark.parametrize("which,line", [("split", "layered fused vs layered split convolutions: MISMATCH"),
+                                        ("flow", "dataflow (banded, one persistent launch) vs layered: MISMATCH"),
+                                        ("band", "banded waves vs layered: MISMATCH"),
+                                        ("oracle", "max coefficient discrepancy")])
+def test_cli_verify_fails_on_a_broken_path(which, line):
+    """verify is not vacuous: a one-ulp change in one path's result (or a
+    1e-6 relative change in every path, against the independent evaluator)
+    turns it into FAIL"""
+    import os
+    import subprocess
+
+    cli = os.path.join(os.path.dirname(pe.LIB_PATH), "pseval_b200")
+    env = dict(os.environ, PSE_VERIFY_PERTURB=which)
+    r = subprocess.run([cli, "verify", "p1", "--degree", "8", "--precision", "4", "--oracle", "on"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 1 and "verify: FAIL" in r.stdout, r.stdout + r.stderr
+    assert line in r.stdout, r.stdout
+    if which == "oracle":
+        assert "MISMATCH" in r.stdout.split("oracle:")[1]
+
+
+def test_cli_verify_refuses_instances_beyond_the_guard():
+    """--oracle on past within_oracle_guard (oracle_direct.cpp:32-39): refused, exit code 2"""
+    import os
+    import subprocess
+
+    cli = os.path.join(os.path.dirname(pe.LIB_PATH), "pseval_b200")
+    r = subprocess.run([cli, "verify", "p3", "--degree", "60", "--precision", "1", "--oracle", "on"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 2 and "refused" in r.stdout, r.stdout + r.stderr
+
+
+def test_device_eval_direct_equals_reference_eval_direct():
+    """pse_eval_direct (the independent evaluator of verify: direct product
+    chains, literal md arithmetic) equals the reference's own eval_direct
+    (oracle_direct.cpp:41-78) bit for bit -- integer and full-precision
+    instances, real and complex, with exponents"""
+    lib = "ref" if po.has_ref() else "port"
+    rng = np.random.default_rng(2024)
+    for it in range(40):
+        p = int_instance(rng, it % 2 == 1, cplx=it % 4 == 3)
+        ref = po.eval_direct(p, lib)
+        vg = pe.eval_direct_packed(p.n, p.d, p.m, "cplx" if p.cplx else "real", p.nvars, p.idx, p.exps,
+                                   p.stat.reshape(p.P * p.m, *p.stat.shape[2:]))
+        assert_bitwise(vg.reshape(ref.shape), ref, f"int instance {it}")
+    for m in LEVELS:
+        for cplx in (False, True):
+            p = md_instance(rng, m, cplx, with_exponents=True)
+            if not pe.within_oracle_guard(p.d, p.nvars, p.exps):
+                continue
+            ref = po.eval_direct(p, lib)
+            vg = pe.eval_direct_packed(p.n, p.d, p.m, "cplx" if cplx else "real", p.nvars, p.idx, p.exps,
+                                       p.stat.reshape(p.P * m, *p.stat.shape[2:]))
+            assert_bitwise(vg.reshape(ref.shape), ref, f"md instance m={m} cplx={cplx}")
 
 
 def test_slot_rewritten_in_a_later_layer_stays_exact():
