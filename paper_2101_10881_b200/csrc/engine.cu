@@ -549,7 +549,7 @@ struct Plan {
     if (nrows_mine == 0 || conv_mode == 1 || multi_writer || nb16 > 32767 ||
         nrows_mine * nb16 * (nb16 + 1) / 2 >= (int64_t(1) << 31))
       return nl;
-    if (conv_mode >= 2) return 0;  // waves, dataflow and CTA-local dataflow take every layer
+    if (conv_mode >= 2 || cta_mode()) return 0;  // waves, dataflow and CTA-local dataflow take every layer
     const int64_t thr = int64_t(sms) * 4 * 128 * 2, npairs = (d + 2) / 2;
     if (static_cast<int64_t>(batch) * layer_pairs < thr) return 0;
     int f = nl;
@@ -576,7 +576,18 @@ struct Plan {
     double makespan = 0;  // simulated, in steps: the slowest group
   } cta;
 
-  bool cta_mode() const { return conv_mode == 4 && cta_ready(); }
+  // The CTA-local path is taken when forced (PSE_CONV_MODE=cta) and, by
+  // default, at M = 1 for deep graphs of few large job groups (a block per
+  // group still fills the GPU, and the group's chains are long): there a
+  // task's arithmetic is a DMUL + DADD per step and the global dataflow
+  // kernel's per-task L2 round trips dominate (C3 / C3' m=1: 0.92 / 1.16 ->
+  // 0.39 ms). Many small groups (p1, p3) stay on the global kernel (C2 m=1:
+  // 0.22 vs 0.61 ms CTA-local); at M >= 2 the global kernel is faster.
+  bool prefer_cta() const {
+    return conv_mode == 4 ||
+           (conv_mode == 0 && m == 1 && ncomps > 0 && ncomps <= 2 * sms && nrows_mine >= int64_t(32) * ncomps);
+  }
+  bool cta_mode() const { return prefer_cta() && cta_ready(); }
   bool cta_ready() const { return cta.built && cta.ok; }
 
   void prepare_cta() {
@@ -632,12 +643,9 @@ struct Plan {
       }
       return worst;
     };
-    if (band_w) {
-      cta.W = band_w;
-    } else {
-      const double m16 = sched_all(16, false), m32 = sched_all(32, false);
-      cta.W = m16 < m32 ? 16 : 32;
-    }
+    // 32-wide bands: a block's warps are few, so fewer, longer tasks win
+    // (C3 m=1: 0.39 ms at W=32 vs 0.78 at 16); PSE_BAND_W overrides
+    cta.W = band_w ? band_w : 32;
     cta.makespan = sched_all(cta.W, true);
     cta.ngroups = static_cast<int>(goff.size()) - 1;
     if (!L->cta_fits(cta.max_units)) return;  // stays on the global dataflow path
@@ -652,7 +660,7 @@ struct Plan {
 
   // host schedule + upload for a batch size (never during stream capture)
   void prepare_band(int batch) {
-    if (conv_mode == 4) {
+    if (prefer_cta()) {
       prepare_cta();
       if (cta_ready()) return;
     }
@@ -1221,7 +1229,7 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
   p->vg = dev_alloc<double>(static_cast<size_t>(p->Q) * max_batch * p->nrows * (g.d + 1));
   ck(cudaStreamSynchronize(s), "plan upload");
 
-  if (p->conv_mode == 4) p->prepare_cta();
+  if (p->prefer_cta()) p->prepare_cta();
   const Costs c = costs(g.m);
   p->flops_model = flop_count(g, 0, c.rep_add, c.rep_mul);
   p->alg_ops = alg_op_count(g);

@@ -215,6 +215,9 @@ struct Launchers {
 
 constexpr int kConvThreads = kLaneThreads;
 constexpr size_t kCtaSmemMax = 227 * 1024;  // dynamic shared memory of one block
+#ifndef PSE_CTA_SLEEP
+#define PSE_CTA_SLEEP 20  // ns between polls of a shared-memory completion flag (0: spin)
+#endif
 // resident blocks per SM for a target expressed in 128-thread blocks (the
 // register budget stays the same whatever the block size)
 constexpr int blocks_for(int minb128) { return minb128 * 128 / kConvThreads > 0 ? minb128 * 128 / kConvThreads : 1; }
@@ -234,12 +237,12 @@ __device__ __forceinline__ void load_md(const double* __restrict__ src, int S, i
 
 // coh: the series may be written during this kernel by other SMs, so it is
 // read through L2 (ld.global.cg) instead of the non-coherent read-only path
-template <int M>
+template <int M, bool CTA = false>
 __device__ __forceinline__ void load_md_sel(const double* __restrict__ src, int S, int j, double (&v)[M], bool coh) {
   const double* p = src + j;
 #pragma unroll
   for (int q = 0; q < M; ++q) {
-    v[q] = coh ? __ldcg(p) : __ldg(p);
+    v[q] = coh ? (CTA ? __ldca(p) : __ldcg(p)) : __ldg(p);
     p += S;
   }
 }
@@ -444,7 +447,18 @@ __host__ __device__ constexpr bool band_stage() {
 // lanes of a task of kind `kind` (band width W)
 __device__ __forceinline__ int band_task_lanes(int kind, int W) { return kind == -2 ? W / 2 : W; }
 
-template <int M, bool CPLX, bool COH>
+// loads of data produced during the launch: through L2 (.cg) when the
+// producer may sit on another SM; through L1 (.ca) when every producer runs
+// on this SM (CTA-local dataflow: the SM's own stores keep its L1 coherent)
+template <bool CTA>
+__device__ __forceinline__ double ld_prod(const double* p) {
+  if constexpr (CTA)
+    return __ldca(p);
+  else
+    return __ldcg(p);
+}
+
+template <int M, bool CPLX, bool COH, bool CTA = false>
 __device__ __forceinline__ void band_task(double* arena, const Geom& G, const int4* __restrict__ jobs,
                                           const int4* __restrict__ slots, int W, int64_t pt, int lane, Lane sm,
                                           double* __restrict__ stg) {
@@ -478,11 +492,11 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
       for (int q = 0; q < Q; ++q) {
         for (int e = lane; e < W; e += 32) {
           const int ix = hxb + e;
-          if (ix <= d) stg[q * kStageSlots + hxo + e] = chx ? __ldcg(Xh + q * S + ix) : __ldg(Xh + q * S + ix);
+          if (ix <= d) stg[q * kStageSlots + hxo + e] = chx ? ld_prod<CTA>(Xh + q * S + ix) : __ldg(Xh + q * S + ix);
         }
         for (int e = lane; e < ny; e += 32) {
           const int iy = hyb + e;
-          if (iy >= 0 && iy <= d) stg[q * kStageSlots + hyo + e] = chy ? __ldcg(Yh + q * S + iy) : __ldg(Yh + q * S + iy);
+          if (iy >= 0 && iy <= d) stg[q * kStageSlots + hyo + e] = chy ? ld_prod<CTA>(Yh + q * S + iy) : __ldg(Yh + q * S + iy);
         }
       }
     }
@@ -523,7 +537,7 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
   const bool cx = COH && (J.w & 2), cy = COH && (J.w & 4);
   if (kind == -3) {  // copy job (executor.cpp:130-133)
 #pragma unroll 1
-    for (int q = 0; q < Q; ++q) Z[q * S + kA] = cx ? __ldcg(X + q * S + kA) : X[q * S + kA];
+    for (int q = 0; q < Q; ++q) Z[q * S + kA] = cx ? ld_prod<CTA>(X + q * S + kA) : X[q * S + kA];
     return;
   }
   // operand loads: limb part*M+q of x_i / y_j
@@ -532,7 +546,7 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
 #pragma unroll
       for (int q = 0; q < M; ++q) v[q] = stg[(part * M + q) * kStageSlots + xo + i - xb];
     } else {
-      load_md_sel<M>(X + part * M * S, S, i, v, cx);
+      load_md_sel<M, CTA>(X + part * M * S, S, i, v, cx);
     }
   };
   auto ldy = [&](int part, int j, double(&v)[M]) {
@@ -540,7 +554,7 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
 #pragma unroll
       for (int q = 0; q < M; ++q) v[q] = stg[(part * M + q) * kStageSlots + yo + j - yb];
     } else {
-      load_md_sel<M>(Y + part * M * S, S, j, v, cy);
+      load_md_sel<M, CTA>(Y + part * M * S, S, j, v, cy);
     }
   };
   const int nA = ibA - iaA + 1;
@@ -563,10 +577,10 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
         gx = true;
         gy = true;
       }
-      auto rx = [&](int s) { return gx ? (cx ? __ldcg(xp + s) : __ldg(xp + s)) : xp[s]; };
-      auto ry = [&](int s) { return gy ? (cy ? __ldcg(yp - s) : __ldg(yp - s)) : yp[-s]; };
+      auto rx = [&](int s) { return gx ? (cx ? ld_prod<CTA>(xp + s) : __ldg(xp + s)) : xp[s]; };
+      auto ry = [&](int s) { return gy ? (cy ? ld_prod<CTA>(yp - s) : __ldg(yp - s)) : yp[-s]; };
       const int n = ib - ia + 1;
-      double acc = ia == 0 ? __dmul_rn(rx(0), ry(0)) : __dadd_rn(__ldcg(Z + k), __dmul_rn(rx(0), ry(0)));
+      double acc = ia == 0 ? __dmul_rn(rx(0), ry(0)) : __dadd_rn(ld_prod<CTA>(Z + k), __dmul_rn(rx(0), ry(0)));
 #pragma unroll 4
       for (int s2 = 1; s2 < n; ++s2) acc = __dadd_rn(acc, __dmul_rn(rx(s2), ry(s2)));
       Z[k] = acc;
@@ -592,7 +606,7 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
       } else {
         if (i == ia) {  // resume the partial sum of the previous segment
 #pragma unroll
-          for (int q = 0; q < M; ++q) o[q] = __ldcg(Z + q * S + k);
+          for (int q = 0; q < M; ++q) o[q] = ld_prod<CTA>(Z + q * S + k);
           acc_store<M>(o, sm);
         }
         acc_add<M>(p, o, sm);
@@ -626,7 +640,7 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
         } else {
           if (i == ia) {  // resume the partial sums of the previous segment
 #pragma unroll
-            for (int q = 0; q < M; ++q) o[q] = __ldcg(Z + q * S + k);
+            for (int q = 0; q < M; ++q) o[q] = ld_prod<CTA>(Z + q * S + k);
             acc_store<M>(o, sm);
           }
           acc_add<M>(pr, o, sm);
@@ -638,7 +652,7 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
         } else {
           if (i == ia) {
 #pragma unroll
-            for (int q = 0; q < M; ++q) ar[q] = __ldcg(Z + q * S + k);
+            for (int q = 0; q < M; ++q) ar[q] = ld_prod<CTA>(Z + q * S + k);
           }
           exp_add_fast<M>(ar, pr, ar, sm);
         }
@@ -655,7 +669,7 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
           store_md<M>(Z + M * S, S, k, pr);
         } else {
 #pragma unroll
-          for (int q = 0; q < M; ++q) ai[q] = __ldcg(Z + (M + q) * S + k);
+          for (int q = 0; q < M; ++q) ai[q] = ld_prod<CTA>(Z + (M + q) * S + k);
           exp_add_fast<M>(ai, pr, ai, sm);
           store_md<M>(Z + M * S, S, k, ai);
         }
@@ -665,7 +679,7 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
         } else {
           if (i == ia) {
 #pragma unroll
-            for (int q = 0; q < M; ++q) ai[q] = __ldcg(Z + (M + q) * S + k);
+            for (int q = 0; q < M; ++q) ai[q] = ld_prod<CTA>(Z + (M + q) * S + k);
           }
           exp_add_fast<M>(ai, pr, ai, sm);
         }
@@ -728,8 +742,20 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// resident blocks per SM the dataflow kernel's registers are budgeted for
+// (PSE_FLOW_MINB_SMALL for M <= 2: their chains are latency-bound and want
+// warps more than registers -- two 512-thread blocks at <= 64 registers:
+// C3 m=2 4.86 -> 4.53 ms)
+#ifndef PSE_FLOW_MINB_SMALL
+#define PSE_FLOW_MINB_SMALL 2
+#endif
+template <int M>
+constexpr int flow_minb() {
+  return M <= 2 ? PSE_FLOW_MINB_SMALL : blocks_for(4);
+}
+
 template <int M, bool CPLX>
-__global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_flow(const FlowArgs a) {
+__global__ void __launch_bounds__(kConvThreads, flow_minb<M>()) k_conv_flow(const FlowArgs a) {
   extern __shared__ double smem[];
   const Lane sm = make_lane(smem);
   const int lane = threadIdx.x & 31;
@@ -805,12 +831,16 @@ __global__ void __launch_bounds__(kConvThreads, 1) k_conv_cta(const CtaArgs a) {
     if (static_cast<int>(u) >= nu) break;
     const int p = u0 + static_cast<int>(u);
     for (int e = a.dep_off[p] + lane; e < a.dep_off[p + 1]; e += 32)
-      while (done[a.deps[e]] == 0) __nanosleep(20);
+      while (done[a.deps[e]] == 0) {
+#if PSE_CTA_SLEEP
+        __nanosleep(PSE_CTA_SLEEP);
+#endif
+      }
     __syncwarp();
     __threadfence_block();
     const int4* slots = a.tasks + static_cast<int64_t>(p) * kSlots;
     const int layer = stamp_slot_layer(a.stamps, a.jobs, slots, lane);
-    band_task<M, CPLX, true>(a.arena, a.G, a.jobs, slots, a.W, pt, lane, sm, stg);
+    band_task<M, CPLX, true, true>(a.arena, a.G, a.jobs, slots, a.W, pt, lane, sm, stg);
     __syncwarp();  // the staging area is rewritten by the next unit
     __threadfence_block();
     if (lane == 0) done[u] = 1;

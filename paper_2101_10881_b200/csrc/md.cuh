@@ -196,6 +196,9 @@ __device__ __noinline__ void exp_mul_lit(const double* x, const double* y, doubl
 #define PSE_LANE_THREADS 128
 #endif
 constexpr int kLaneThreads = PSE_LANE_THREADS;
+#ifndef PSE_PUSH_PRED
+#define PSE_PUSH_PRED 0
+#endif
 constexpr unsigned kRow = kLaneThreads * sizeof(double);  // bytes between rows
 
 // A thread's private shared-memory lane: row r at byte address base + r*kRow.
@@ -495,6 +498,20 @@ __device__ __forceinline__ void push(Passes& st, double v, unsigned lim) {
   // store, then advance top by one row iff v != 0 (either sign): written in
   // PTX so ptxas emits a predicated add (STS + LOP3.P + @P IADD)
   const unsigned addr = CLAMP ? min(st.top, lim) : st.top;
+#if PSE_PUSH_PRED
+  // only nonzero terms are stored (about a quarter of them): less shared-
+  // memory traffic, the store waiting on the zero test
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, t;\n\t"
+      "mov.b64 {lo, hi}, %2;\n\t"
+      "and.b32 t, hi, 0x7fffffff;\n\t"
+      "or.b32 t, t, lo;\n\t"
+      "setp.ne.u32 p, t, 0;\n\t"
+      "@p st.shared.f64 [%1], %2;\n\t"
+      "@p add.u32 %0, %0, %3;\n\t}"
+      : "+r"(st.top)
+      : "r"(addr), "d"(v), "n"(kRow));
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, t;\n\t"
       "st.shared.f64 [%1], %2;\n\t"
@@ -505,6 +522,7 @@ __device__ __forceinline__ void push(Passes& st, double v, unsigned lim) {
       "@p add.u32 %0, %0, %3;\n\t}"
       : "+r"(st.top)
       : "r"(addr), "d"(v), "n"(kRow));
+#endif
 }
 
 // pass-1 step on term t (terms arrive t[n-2], t[n-3], ..., t[0]) followed by
