@@ -351,6 +351,49 @@ __device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm)
       }
       if (i == kk) store_md<M>(Z, S, kk, o);
     }
+  } else if constexpr (cplx_acc_lane<M>()) {
+    // Complex, M >= 5: two passes over the coefficient chains -- the real
+    // parts (re = mul(xr,yr) - mul(xi,yi), acc_re += re), then the imaginary
+    // parts (im = mul(xr,yi) + mul(xi,yr), acc_im += im) -- through ONE loop
+    // body of two md_muls, the accumulator in the lane. The reference's
+    // per-product order (pseries.cpp:49-59) is kept within each part and the
+    // two accumulations are independent, so the results are the same bits;
+    // one operand pair and one accumulator are live at a time (no spills) and
+    // the loop carries two inlined md_muls instead of four.
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      acc_init<M>(sm);
+      double* Zp = Z + part * M * S;
+      const double* Y1 = part ? Y + M * S : Y;  // y of the first product: yr (re) / yi (im)
+      const double* Y2 = part ? Y : Y + M * S;  // y of the second: yi (re) / yr (im)
+      const int sgn = part ? 0 : static_cast<int>(0x80000000u);
+#pragma unroll 1
+      for (int t = 0; t < total; ++t) {
+        const bool second = t >= n1;
+        const int kk = second ? k2 : k1;
+        const int i = second ? t - n1 : t;
+        double xa[M], yb[M], p1[M], p2[M], pr[M];
+        load_md<M>(X, S, i, xa);
+        load_md<M>(Y1, S, kk - i, yb);
+        exp_mul_fast<M>(xa, yb, p1, sm);  // xr * yr | xr * yi
+        load_md<M>(X + M * S, S, i, xa);
+        load_md<M>(Y2, S, kk - i, yb);
+        exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yi | xi * yr
+        // md_sub = exp_add of the negation (expansion.hpp:160-170): flip the
+        // sign bits for the real part, branch-free
+#pragma unroll
+        for (int q = 0; q < M; ++q)
+          p2[q] = __hiloint2double(__double2hiint(p2[q]) ^ sgn, __double2loint(p2[q]));
+        exp_add_fast<M>(p1, p2, pr, sm);
+        if (i == 0) {
+          copy_md<M>(p1, pr);
+          acc_store<M>(pr, sm);
+        } else {
+          acc_add<M>(pr, p1, sm);
+        }
+        if (i == kk) store_md<M>(Zp, S, kk, p1);
+      }
+    }
   } else {
     // accumulators (re, im). For M >= 5 the real one lives in the lane
     // (cplx_acc_lane), so its M registers are free while the four md_muls
@@ -613,8 +656,47 @@ __device__ __forceinline__ void band_task(double* arena, const Geom& G, const in
       }
       if (i == (second ? ibB : ibA)) store_md<M>(Z, S, k, o);
     }
+  } else if constexpr (cplx_acc_lane<M>()) {
+    // as k_conv's complex branch for M >= 5: the real parts, then the
+    // imaginary parts, one two-md_mul loop body, the accumulator in the lane
+#pragma unroll 1
+    for (int part = 0; part < 2; ++part) {
+      acc_init<M>(sm);
+      const int sgn = part ? 0 : static_cast<int>(0x80000000u);
+      double o[M];
+#pragma unroll 1
+      for (int t = 0; t < total; ++t) {
+        const bool second = t >= nA;
+        const int k = second ? kB : kA;
+        const int ia = second ? iaB : iaA;
+        const int i = second ? iaB + (t - nA) : iaA + t;
+        double xa[M], yb[M], p1[M], p2[M], pr[M];
+        ldx(0, i, xa);
+        ldy(part, k - i, yb);
+        exp_mul_fast<M>(xa, yb, p1, sm);  // xr * yr | xr * yi
+        ldx(1, i, xa);
+        ldy(1 - part, k - i, yb);
+        exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yi | xi * yr
+#pragma unroll
+        for (int q = 0; q < M; ++q)  // md_sub for the real part (expansion.hpp:160-170)
+          p2[q] = __hiloint2double(__double2hiint(p2[q]) ^ sgn, __double2loint(p2[q]));
+        exp_add_fast<M>(p1, p2, pr, sm);
+        if (i == 0) {
+          copy_md<M>(o, pr);
+          acc_store<M>(pr, sm);
+        } else {
+          if (i == ia) {  // resume the partial sum of the previous segment
+#pragma unroll
+            for (int q = 0; q < M; ++q) o[q] = ld_prod<CTA>(Z + (part * M + q) * S + k);
+            acc_store<M>(o, sm);
+          }
+          acc_add<M>(pr, o, sm);
+        }
+        if (i == (second ? ibB : ibA)) store_md<M>(Z + part * M * S, S, k, o);
+      }
+    }
   } else {
-    // as k_conv's complex branch (real accumulator in the lane for M >= 5)
+    // complex, M < 5: both accumulators in registers
     constexpr bool LANE_RE = cplx_acc_lane<M>();
     double ar[LANE_RE ? 1 : M], ai[M], o[M];
     if constexpr (LANE_RE) acc_init<M>(sm);
@@ -746,12 +828,12 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // (PSE_FLOW_MINB_SMALL for M <= 2: their chains are latency-bound and want
 // warps more than registers -- two 512-thread blocks at <= 64 registers:
 // C3 m=2 4.86 -> 4.53 ms)
-#ifndef PSE_FLOW_MINB_SMALL
-#define PSE_FLOW_MINB_SMALL 2
+#ifndef PSE_FLOW_MINB128_SMALL
+#define PSE_FLOW_MINB128_SMALL 8  // in 128-thread blocks: 32 warps per SM at <= 64 registers
 #endif
 template <int M>
 constexpr int flow_minb() {
-  return M <= 2 ? PSE_FLOW_MINB_SMALL : blocks_for(4);
+  return M <= 2 ? blocks_for(PSE_FLOW_MINB128_SMALL) : blocks_for(4);
 }
 
 template <int M, bool CPLX>
