@@ -824,20 +824,8 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// resident blocks per SM the dataflow kernel's registers are budgeted for
-// (PSE_FLOW_MINB_SMALL for M <= 2: their chains are latency-bound and want
-// warps more than registers -- two 512-thread blocks at <= 64 registers:
-// C3 m=2 4.86 -> 4.53 ms)
-#ifndef PSE_FLOW_MINB128_SMALL
-#define PSE_FLOW_MINB128_SMALL 8  // in 128-thread blocks: 32 warps per SM at <= 64 registers
-#endif
-template <int M>
-constexpr int flow_minb() {
-  return M <= 2 ? blocks_for(PSE_FLOW_MINB128_SMALL) : blocks_for(4);
-}
-
 template <int M, bool CPLX>
-__global__ void __launch_bounds__(kConvThreads, flow_minb<M>()) k_conv_flow(const FlowArgs a) {
+__global__ void __launch_bounds__(kConvThreads, blocks_for(4)) k_conv_flow(const FlowArgs a) {
   extern __shared__ double smem[];
   const Lane sm = make_lane(smem);
   const int lane = threadIdx.x & 31;

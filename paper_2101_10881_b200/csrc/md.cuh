@@ -199,9 +199,6 @@ constexpr int kLaneThreads = PSE_LANE_THREADS;
 #ifndef PSE_PUSH_PRED
 #define PSE_PUSH_PRED 1
 #endif
-#ifndef PSE_REG_MD2
-#define PSE_REG_MD2 1  // register-only exp_add / exp_mul at M = 2
-#endif
 constexpr unsigned kRow = kLaneThreads * sizeof(double);  // bytes between rows
 
 // A thread's private shared-memory lane: row r at byte address base + r*kRow.
@@ -442,103 +439,12 @@ __device__ __forceinline__ void exp_add_core(double xh, double xn, double yh, do
   tighten_fast<M>(out);
 }
 
-// ------------------------------------------------ register-only M = 2
-// At M = 2 every stage of exp_add / exp_mul fits in registers: the merge is
-// the reference's greedy merge written out as its decision tree (exact for
-// any operands, sorted or not), vec_sum and vec_sum_err_branch run over
-// register arrays with the emissions selected into place (zero terms are
-// processed, exactly as the reference does), and nothing touches shared
-// memory -- no lane stores, no load-dependent merge chain.
-
-// vec_sum_err_branch (expansion.hpp:74-90) over n register terms, M = 2
-// outputs. After the second emission the reference returns; later steps
-// here cannot write out (j >= 2) and eps is then unused.
-template <int N>
-__device__ __forceinline__ void err_branch2(const double (&e)[N], double (&out)[2]) {
-  double eps = e[0];
-  int j = 0;
-  out[0] = 0.0;
-  out[1] = 0.0;
-#pragma unroll
-  for (int i = 1; i < N; ++i) {
-    double r, t;
-    fast_two_sum(eps, e[i], r, t);
-    const bool nz = t != 0.0;
-    out[0] = (nz && j == 0) ? r : out[0];
-    out[1] = (nz && j == 1) ? r : out[1];
-    eps = nz ? t : r;
-    j += nz ? 1 : 0;
-  }
-  // out[j++] = eps; then zero padding (already zero)
-  out[0] = j == 0 ? eps : out[0];
-  out[1] = j == 1 ? eps : out[1];
-}
-
-// exp_add<2> (expansion.hpp:142-158), registers only
-__device__ __forceinline__ void exp_add_reg2(const double (&x)[2], const double (&y)[2], double (&out)[2]) {
-  // greedy merge by magnitude, ties take x (expansion.hpp:150-153)
-  const bool c00 = fabs(x[0]) >= fabs(y[0]), c10 = fabs(x[1]) >= fabs(y[0]);
-  const bool c01 = fabs(x[0]) >= fabs(y[1]), c11 = fabs(x[1]) >= fabs(y[1]);
-  const double m2 = c11 ? x[1] : y[1], m3 = c11 ? y[1] : x[1];
-  double t[4];
-  t[0] = c00 ? x[0] : y[0];
-  t[1] = c00 ? (c10 ? x[1] : y[0]) : (c01 ? x[0] : y[1]);
-  t[2] = c00 ? (c10 ? y[0] : m2) : (c01 ? m2 : x[0]);
-  t[3] = c00 ? (c10 ? y[1] : m3) : (c01 ? m3 : x[1]);
-  // vec_sum (expansion.hpp:61-69)
-  double s = t[3];
-#pragma unroll
-  for (int q = 2; q >= 0; --q) {
-    double e;
-    two_sum(t[q], s, s, e);
-    t[q + 1] = e;
-  }
-  t[0] = s;
-  err_branch2<4>(t, out);
-  tighten_fast<2>(out);
-}
-
-// exp_mul<2> (expansion.hpp:177-211), registers only: NT = 7 terms in the
-// reference's order [p00 | e00 p01 p10 | e01 e10 p11 p... ] built exactly as
-// the reference loop does
-__device__ __forceinline__ void exp_mul_reg2(const double (&x)[2], const double (&y)[2], double (&out)[2]) {
-  double t[7];
-  double p00, e00, p01, e01, p10, e10;
-  two_prod(x[0], y[0], p00, e00);  // diagonal 0
-  two_prod(x[0], y[1], p01, e01);  // diagonal 1
-  two_prod(x[1], y[0], p10, e10);
-  // k = 0: [p00], carry {e00}; k = 1: [p01 p10] + carry e00, carry {e01 e10};
-  // k = 2 (= M): plain x1*y1 + carry e01 e10
-  t[0] = p00;
-  t[1] = p01;
-  t[2] = p10;
-  t[3] = e00;
-  t[4] = __dmul_rn(x[1], y[1]);
-  t[5] = e01;
-  t[6] = e10;
-#pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-    double s = t[6];
-#pragma unroll
-    for (int q = 5; q >= 0; --q) {
-      double e;
-      two_sum(t[q], s, s, e);
-      t[q + 1] = e;
-    }
-    t[0] = s;
-  }
-  err_branch2<7>(t, out);
-  tighten_fast<2>(out);
-}
-
 // out = x + y (expansion.hpp:142-158), operands in registers. Safe for out
 // aliasing x or y.
 template <int M, bool LAT = false>
 __device__ __forceinline__ void exp_add_fast(const double (&x)[M], const double (&y)[M], double (&out)[M], Lane ln) {
   if constexpr (M == 1) {
     out[0] = __dadd_rn(x[0], y[0]);
-  } else if constexpr (M == 2 && PSE_REG_MD2) {
-    exp_add_reg2(x, y, out);
   } else {
 #pragma unroll
     // x at rows 0..M-1 + NaN sentinel at row M, y at rows M+1..2M + zero
@@ -637,8 +543,6 @@ template <int M>
 __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double (&y)[M], double (&out)[M], Lane ln) {
   if constexpr (M == 1) {
     out[0] = __dmul_rn(x[0], y[0]);
-  } else if constexpr (M == 2 && PSE_REG_MD2) {
-    exp_mul_reg2(x, y, out);
   } else {
     constexpr int CAP = MdTraits<M>::CAP;
     const unsigned lim = ln.base + CAP * kRow;
