@@ -5,7 +5,11 @@
 // against four 128-thread blocks); the register and shared-memory budget per
 // thread is unchanged. M <= 2 keeps 128: its lighter threads fit more warps.
 #ifndef PSE_LANE_THREADS
+#ifdef PSE_M8_THREADS
+#define PSE_LANE_THREADS PSE_M8_THREADS
+#else
 #define PSE_LANE_THREADS 512
+#endif
 #endif
 #include "kernels.cuh"
 
