@@ -891,14 +891,17 @@ struct Plan {
       conv_layer_ms[l] = at ? ms(at, e) : 0.0;
       at = e;
     }
-    const Stamp conv_end = at;
+    Stamp conv_end = at;
     add_layer_ms.assign(n_add_layers, 0.0);
     double scale = 0, add = 0;
     Stamp tail_end = conv_end;
     if (tail) {
       // a sharded plan's tail starts after the exchange (barriers + gather);
-      // otherwise the launch gap belongs to the first tail phase
+      // otherwise the launch gap belongs to the first tail phase. A rank
+      // without conv jobs (more ranks than job groups) has no conv stage:
+      // its evaluation starts with the tail.
       const Stamp tb = h[1 + n_conv_layers] ? ~h[1 + n_conv_layers] : conv_end;
+      if (!h[0]) conv_end = tb;
       at = nranks > 1 ? std::max(tb, conv_end) : conv_end;
       exchange_ms = nranks > 1 ? ms(conv_end, at) : 0.0;
       if (nts) {
@@ -920,7 +923,7 @@ struct Plan {
       rep->conv_ms = conv;
       rep->scale_ms = scale;
       rep->add_ms = add;
-      rep->wall_ms = h[0] ? ms(t0, tail_end) : scale + add;
+      rep->wall_ms = h[0] ? ms(t0, tail_end) : exchange_ms + scale + add;
     }
   }
 

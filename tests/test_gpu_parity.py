@@ -674,3 +674,30 @@ def test_sharded_report_times_the_exchange_on_the_device():
         fin = p.finish(1)
         assert fin.conv_ms > 0 and fin.add_ms > 0 and fin.exchange_ms >= 0
         assert abs(fin.conv_ms + fin.exchange_ms + fin.scale_ms + fin.add_ms - fin.wall_ms) <= 1e-6 * fin.wall_ms + 1e-6
+
+
+def test_sharded_plan_with_an_empty_rank():
+    """more ranks than independent job groups (one monomial, 3 ranks): the
+    ranks without conv jobs still run the exchange and the exact addition
+    tree, and every rank's result equals one device's"""
+    pe_g = pe.GraphArrays  # noqa: F841 (import check)
+    rng = np.random.default_rng(11)
+    p = md_instance(rng, 2, False, nmax=3, Nmax=1, dmin=5, dmax=5)
+    g = pe.build_jobgraph_shape(p.n, p.d, p.nvars, p.idx)
+    st = p.stat.reshape(p.P * p.m, *p.stat.shape[2:])
+    want, _, _ = pe.DevicePlan(g, 2, "real", 0, 1).run(st, 1)
+    plans = [pe.DevicePlan(g, 2, "real", 0, 1, rank=r, nranks=3) for r in range(3)]
+    for p1 in plans:
+        for p2 in plans:
+            if p2 is not p1:
+                p1.set_peer(p2.rank, p2)
+        p1.upload(st, 1)
+        rep = p1.execute(1)
+        assert rep.conv_ms >= 0
+    for p1 in plans:
+        p1.gather_peers(1)
+    for p1 in plans:
+        fin = p1.finish(1)
+        assert fin.add_ms >= 0 and fin.wall_ms >= 0
+        vg, _ = p1.download(1)
+        assert_bitwise(vg, want, f"rank {p1.rank}/3 of a one-monomial polynomial")
