@@ -307,6 +307,17 @@ CONV_KERNEL = {
 }
 
 
+def repeat_count(t_eval_ms: float, red_dev=None) -> int:
+    """Evaluations per timed step: short evaluations repeat so that a step
+    lasts >= 25 ms and the clock sampler sees it (C1, small precisions). The
+    count is the max over ranks -- every rank must run the same number of
+    evaluations, since a sharded evaluation has collectives."""
+    from paper_2101_10881_b200 import dist as D
+
+    mine = max(1, int(np.ceil(25.0 / max(t_eval_ms, 1e-3))))
+    return int(D.max_over_ranks(float(mine), red_dev))
+
+
 def gpu_setup(args):
     import torch
 
@@ -401,8 +412,9 @@ def ours_points(args, wl):
     for _ in range(args.warmup):
         t_eval = evaluate_once()[0]
     # short evaluations repeat inside a step so that every step lasts >= 25 ms
-    # and the clock sampler sees the timed region (C1, small precisions)
-    reps = max(1, int(np.ceil(25.0 / max(t_eval, 1e-3))))
+    # and the clock sampler sees the timed region (C1, small precisions); the
+    # same count on every rank
+    reps = repeat_count(t_eval, red_dev)
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
@@ -512,7 +524,8 @@ def ours_monomials(args, wl):
 
     for _ in range(args.warmup):
         t_eval = evaluate_once()[0]
-    reps = max(1, int(np.ceil(25.0 / max(t_eval, 1e-3))))
+    # the same repeat count on every rank: each evaluation has collectives
+    reps = repeat_count(t_eval, red_dev)
     if world > 1:
         torch.distributed.barrier()
     walls, convs, exs, launches = [], [], [], 0

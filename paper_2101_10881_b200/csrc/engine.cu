@@ -610,15 +610,14 @@ struct Plan {
     const double ovh = 250.0 / static_cast<double>(cst.inst_mul + cst.inst_add);
     std::vector<int4> jobs, tasks;
     std::vector<int> goff(1, 0), doff(1, 0), deps;
-    auto sched_all = [&](int W, bool commit) {
+    for (int c = 0; c < ncomps; ++c)  // a group too large to schedule stays on the global path
+      if (static_cast<int64_t>(rows[c].size()) * nb16 * (nb16 + 1) / 2 >= (int64_t(1) << 31)) return;
+    auto sched_all = [&](int W) {
       double worst = 0;
       for (int c = 0; c < ncomps; ++c) {
         if (rows[c].empty()) continue;
-        if (static_cast<int64_t>(rows[c].size()) * nb16 * (nb16 + 1) / 2 >= (int64_t(1) << 31))
-          throw std::invalid_argument("job group too large for the banded schedule");
         const BandSched sc = band_schedule(rows[c], d, W, kSlots, true, int64_t(warps) * (32 / W), flow_slack, ovh);
         worst = std::max(worst, sc.makespan);
-        if (!commit) continue;
         const int jbase = static_cast<int>(jobs.size());
         std::set<int64_t> produced;
         for (auto& r : rows[c]) produced.insert(r.out);
@@ -646,7 +645,7 @@ struct Plan {
     // 32-wide bands: a block's warps are few, so fewer, longer tasks win
     // (C3 m=1: 0.39 ms at W=32 vs 0.78 at 16); PSE_BAND_W overrides
     cta.W = band_w ? band_w : 32;
-    cta.makespan = sched_all(cta.W, true);
+    cta.makespan = sched_all(cta.W);
     cta.ngroups = static_cast<int>(goff.size()) - 1;
     if (!L->cta_fits(cta.max_units)) return;  // stays on the global dataflow path
     cta.jobs = dev_upload(jobs, stream);

@@ -139,3 +139,30 @@ def test_connect_peers_exchanges_handles_and_agrees_on_fallback(fail_rank):
         assert v[0] == (fail_rank < 0)
         if fail_rank < 0:
             assert [int(x) for x in v[1:]] == [0 if q == r else q + 1 for q in range(world)]
+
+
+def _reps_worker(rank, world, port, outdir):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    import bench
+    from paper_2101_10881_b200 import dist as DD
+
+    dist = DD.init("gloo")
+    # ranks measure different evaluation times; a sharded evaluation has
+    # collectives, so every rank must repeat it the same number of times
+    reps = bench.repeat_count([0.2, 5.0][rank % 2])
+    np.save(os.path.join(outdir, f"reps{rank}.npy"), np.array([reps]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_bench_repeat_count_agrees_across_ranks():
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_reps_worker, args=(2, _free_port(), tmp), nprocs=2, join=True)
+        reps = [int(np.load(os.path.join(tmp, f"reps{r}.npy"))[0]) for r in range(2)]
+    assert reps == [125, 125]
