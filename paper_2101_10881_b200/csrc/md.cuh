@@ -200,6 +200,10 @@ constexpr int kLaneThreads = PSE_LANE_THREADS;
 #define PSE_PUSH_PRED 1
 #endif
 constexpr unsigned kRow = kLaneThreads * sizeof(double);  // bytes between rows
+#ifndef PSE_MERGE_RELOAD
+#define PSE_MERGE_RELOAD 1
+#endif
+constexpr bool kMergeReload = PSE_MERGE_RELOAD;  // exp_add merge: heads re-read (else carried)
 
 // A thread's private shared-memory lane: row r at byte address base + r*kRow.
 struct Lane {
@@ -327,13 +331,21 @@ __device__ __forceinline__ bool tighten_fixed(const double (&w)[M]) {
 }
 
 // tighten (expansion.hpp:92-114): at most M passes, stop at the first pass
-// that changes nothing. Testing "would this pass change nothing" first
+// that changes nothing. Testing "would the next pass change nothing"
 // (tighten_fixed) replaces that final no-op pass -- 9 independent DADDs
 // instead of 9 chained two_sums -- with identical results.
-template <int M>
+template <int M, bool PF>
 __device__ __forceinline__ void tighten_fast(double (&w)[M]) {
+  // PF: the first pass runs unconditionally. On a fixed point a pass changes
+  // nothing (see tighten_fixed), so this only skips the first test; the
+  // remaining M-1 passes keep the test -- same passes, same bits. It pays
+  // where a warp nearly always has a lane that needs the pass: md_add
+  // outputs (M = 2 / 3 / 10: 8 / 16 / 46% of them need one) and md_mul
+  // outputs from M = 5 (M = 3 / 4 / 5 / 10: 0 / 5 / 9.5 / 29%;
+  // tools/md_stats.c).
+  if constexpr (PF) tighten_pass<M>(w);
 #pragma unroll 1
-  for (int pass = 0; pass < M; ++pass) {
+  for (int pass = PF ? 1 : 0; pass < M; ++pass) {
     if (tighten_fixed<M>(w)) return;
     tighten_pass<M>(w);
   }
@@ -380,17 +392,35 @@ __device__ __forceinline__ void exp_add_core(double xh, double xn, double yh, do
     // within 2M steps, so the comparison alone replays the reference's
     // merge and tail copies. (NaN data is outside the bit-exact contract:
     // NaN bit patterns already differ between the host and the device.)
-    unsigned xa = ln.base + (XR + 1) * kRow, ya = ln.base + (YR + 1) * kRow;
+    if constexpr (kMergeReload) {
+      // both heads re-read from the lane after every step (one of the two
+      // loads is redundant): fewer selects than carrying them in registers
+      // (C2 -1.6% in tools/step_bench.cu)
+      unsigned xa = ln.base + XR * kRow, ya = ln.base + YR * kRow;
 #pragma unroll
-    for (int p = 0; p < 2 * M; ++p) {
-      const bool take_x = fabs(xh) >= fabs(yh);
-      t[p] = take_x ? xh : yh;
-      if (p + 1 < 2 * M) {
-        const double v = lds64(take_x ? xa : ya);
-        xh = take_x ? v : xh;
-        yh = take_x ? yh : v;
-        xa += take_x ? kRow : 0u;
-        ya += take_x ? 0u : kRow;
+      for (int p = 0; p < 2 * M; ++p) {
+        const bool take_x = fabs(xh) >= fabs(yh);
+        t[p] = take_x ? xh : yh;
+        if (p + 1 < 2 * M) {
+          xa += take_x ? kRow : 0u;
+          ya += take_x ? 0u : kRow;
+          xh = lds64(xa);
+          yh = lds64(ya);
+        }
+      }
+    } else {
+      unsigned xa = ln.base + (XR + 1) * kRow, ya = ln.base + (YR + 1) * kRow;
+#pragma unroll
+      for (int p = 0; p < 2 * M; ++p) {
+        const bool take_x = fabs(xh) >= fabs(yh);
+        t[p] = take_x ? xh : yh;
+        if (p + 1 < 2 * M) {
+          const double v = lds64(take_x ? xa : ya);
+          xh = take_x ? v : xh;
+          yh = take_x ? yh : v;
+          xa += take_x ? kRow : 0u;
+          ya += take_x ? 0u : kRow;
+        }
       }
     }
   } else {
@@ -436,7 +466,7 @@ __device__ __forceinline__ void exp_add_core(double xh, double xn, double yh, do
     constexpr int q = decltype(qc)::value;
     out[q] = lds64_at_if<q * kRow, q * kRow>(ln.base, jb);
   });
-  tighten_fast<M>(out);
+  tighten_fast<M, true>(out);
 }
 
 // out = x + y (expansion.hpp:142-158), operands in registers. Safe for out
@@ -615,34 +645,35 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
     if (count <= CAP) {
       // vec_sum_err_branch over the compacted terms (popped top-down, one
       // row of look-ahead); emission jj overwrites row count-1-jj, which has
-      // already been consumed
-      // Continue while terms are left and fewer than M were emitted; two
-      // pops per trip with a test between them (no register rotation). The
-      // look-ahead load may read the spare row -1, never below.
+      // already been consumed. Two pops per trip; the emission count is
+      // tested once per trip, so a trip may pop one term after the M-th
+      // emission (where the reference returns): that emission lands in a
+      // row that is never read and eps is then unused. The look-ahead load
+      // may read the spare row -1, never below.
       double eps = st.s2;
       unsigned a = st.top - kRow;        // row of the next term to pop
       unsigned ea = st.top - kRow;       // row of the next emission
-      const unsigned elim = st.top - (M + 1) * kRow;  // ea == elim <=> M emitted
+      const unsigned elim = st.top - (M + 1) * kRow;  // ea <= elim <=> M emitted
       const unsigned base1 = ln.base + kRow;
       double n0 = lds64(a);
 #pragma unroll 1
-      while (a >= ln.base && ea != elim) {
+      while (a >= ln.base && ea > elim) {
         const double n1 = lds64_at<-static_cast<int>(kRow)>(a);  // row a-1 >= spare row
         emit_step<true>(eps, n0, ea);
-        if (a < base1 || ea == elim) break;
+        if (a < base1) break;
         n0 = lds64_at<-2 * static_cast<int>(kRow)>(a);  // row a-2 >= spare row (a-1 >= base)
         emit_step<true>(eps, n1, ea);
         a -= 2 * kRow;
       }
       // emission k sits at row top-1-k; eps goes to the next emission row
-      // (rows below the stack are never reached: ea >= top-(M+1) rows >= -1)
+      // (at most M+1 and at most `count` emissions: ea >= the spare row -1)
       sts64(ea, eps);
       const unsigned jb = st.top - kRow - ea;  // jj rows, in bytes
       static_for<M>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
         out[k] = lds64_at_if<-(k + 1) * static_cast<int>(kRow), k * kRow>(st.top, jb);
       });
-      tighten_fast<M>(out);
+      tighten_fast<M, (M >= 5)>(out);
     } else {
       // rare: more nonzero terms than the lane holds -> literal algorithm
       double xl[M], yl[M], ol[M];
