@@ -214,6 +214,7 @@ struct Launchers {
 #ifdef PSE_KERNELS_IMPL
 
 constexpr int kConvThreads = kLaneThreads;
+
 constexpr size_t kCtaSmemMax = 227 * 1024;  // dynamic shared memory of one block
 #ifndef PSE_CTA_SLEEP
 #define PSE_CTA_SLEEP 20  // ns between polls of a shared-memory completion flag (0: spin)

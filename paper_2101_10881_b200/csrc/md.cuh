@@ -518,6 +518,7 @@ namespace detail {
 struct Passes {
   double s1, s2;
   unsigned top;
+  unsigned step;  // kRow, held in a register (see push)
 };
 
 // push v if nonzero; `clamp` (pushes beyond the first CAP) redirects the
@@ -541,7 +542,7 @@ __device__ __forceinline__ void push(Passes& st, double v, unsigned lim) {
       "@p st.shared.f64 [%1], %2;\n\t"
       "@p add.u32 %0, %0, %3;\n\t}"
       : "+r"(st.top)
-      : "r"(addr), "d"(v), "n"(kRow));
+      : "r"(addr), "d"(v), "r"(st.step));
 #else
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, t;\n\t"
@@ -578,6 +579,12 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
     const unsigned lim = ln.base + CAP * kRow;
     detail::Passes st;
     st.top = ln.base;
+    // the row step from the block size (every lane kernel runs kLaneThreads
+    // threads per block): ptxas cannot turn it back into an immediate, so
+    // each push's predicated advance reads it from a register instead of
+    // re-materialising the constant for every push (-70 instructions per
+    // md_mul at M = 10)
+    asm("{\n\t.reg .b32 n;\n\tmov.u32 n, %%ntid.x;\n\tshl.b32 %0, n, 3;\n\t}" : "=r"(st.step));
     // Pass 2 runs one term behind pass 1: the pass-1 error of term i is
     // consumed by pass 2 while pass 1 processes term i+1, so the two
     // two_sums of a step are independent and interleave (ILP 2). The
