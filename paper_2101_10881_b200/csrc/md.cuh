@@ -208,12 +208,20 @@ constexpr bool kMergeReload = PSE_MERGE_RELOAD;  // exp_add merge: heads re-read
 // A thread's private shared-memory lane: row r at byte address base + r*kRow.
 struct Lane {
   unsigned base;
+  unsigned step;  // kRow, held in a register (see make_lane)
 };
 
 // Row -1 (the first row of the allocation) is a spare: look-ahead loads may
 // touch it harmlessly.
 __device__ __forceinline__ Lane make_lane(double* smem) {
-  return Lane{static_cast<unsigned>(__cvta_generic_to_shared(smem + kLaneThreads + threadIdx.x))};
+  // The row step comes from the block size (every lane kernel runs
+  // kLaneThreads threads per block), so ptxas cannot turn it back into an
+  // immediate: the predicated row advances (stack pushes, emissions, merge
+  // pointers) then read it from one register instead of re-materialising
+  // the constant before each of them.
+  unsigned step;
+  asm("{\n\t.reg .b32 n;\n\tmov.u32 n, %%ntid.x;\n\tshl.b32 %0, n, 3;\n\t}" : "=r"(step));
+  return Lane{static_cast<unsigned>(__cvta_generic_to_shared(smem + kLaneThreads + threadIdx.x)), step};
 }
 
 // volatile: the stack's stores and loads must keep their program order
@@ -261,21 +269,37 @@ __device__ __forceinline__ bool nonzero(double v) {
 // stored at row ea, ea moves one row (down when DOWN) and eps = tt, otherwise
 // eps = r. In PTX so the store, the row advance and the eps select all hang
 // off one predicate (LOP3.P, @P STS, @P IADD, 2 SEL).
+// The row advance is `step` (a register: see make_lane) upward, or the
+// immediate -kRow downward (ptxas emits a predicated VIADD for that one).
 template <bool DOWN>
-__device__ __forceinline__ void emit_step(double& eps, double v, unsigned& ea) {
+__device__ __forceinline__ void emit_step(double& eps, double v, unsigned& ea, unsigned step) {
   double r, tt;
   fast_two_sum(eps, v, r, tt);
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, t;\n\t"
-      "mov.b64 {lo, hi}, %3;\n\t"
-      "and.b32 t, hi, 0x7fffffff;\n\t"
-      "or.b32 t, t, lo;\n\t"
-      "setp.ne.u32 p, t, 0;\n\t"
-      "@p st.shared.f64 [%1], %2;\n\t"
-      "@p add.u32 %1, %1, %4;\n\t"
-      "selp.f64 %0, %3, %2, p;\n\t}"
-      : "=d"(eps), "+r"(ea)
-      : "d"(r), "d"(tt), "n"(DOWN ? 0u - kRow : kRow));
+  if constexpr (DOWN) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, t;\n\t"
+        "mov.b64 {lo, hi}, %3;\n\t"
+        "and.b32 t, hi, 0x7fffffff;\n\t"
+        "or.b32 t, t, lo;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "@p st.shared.f64 [%1], %2;\n\t"
+        "@p add.u32 %1, %1, %4;\n\t"
+        "selp.f64 %0, %3, %2, p;\n\t}"
+        : "=d"(eps), "+r"(ea)
+        : "d"(r), "d"(tt), "n"(0u - kRow));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, t;\n\t"
+        "mov.b64 {lo, hi}, %3;\n\t"
+        "and.b32 t, hi, 0x7fffffff;\n\t"
+        "or.b32 t, t, lo;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "@p st.shared.f64 [%1], %2;\n\t"
+        "@p add.u32 %1, %1, %4;\n\t"
+        "selp.f64 %0, %3, %2, p;\n\t}"
+        : "=d"(eps), "+r"(ea)
+        : "d"(r), "d"(tt), "r"(step));
+  }
 }
 
 // bitwise inequality accumulator: d |= bits(a) ^ bits(b)
@@ -402,8 +426,11 @@ __device__ __forceinline__ void exp_add_core(double xh, double xn, double yh, do
         const bool take_x = fabs(xh) >= fabs(yh);
         t[p] = take_x ? xh : yh;
         if (p + 1 < 2 * M) {
-          xa += take_x ? kRow : 0u;
-          ya += take_x ? 0u : kRow;
+          // one predicated add per pointer (a select would cost two)
+          asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+              "@p add.u32 %0, %0, %3;\n\t@!p add.u32 %1, %1, %3;\n\t}"
+              : "+r"(xa), "+r"(ya)
+              : "r"(static_cast<unsigned>(take_x)), "r"(ln.step));
           xh = lds64(xa);
           yh = lds64(ya);
         }
@@ -457,7 +484,7 @@ __device__ __forceinline__ void exp_add_core(double xh, double xn, double yh, do
   unsigned ea = ln.base;
   double eps = t[0];
 #pragma unroll
-  for (int q = 1; q < 2 * M; ++q) emit_step<false>(eps, t[q], ea);
+  for (int q = 1; q < 2 * M; ++q) emit_step<false>(eps, t[q], ea, ln.step);
   // rows 0..jj-1 hold the emissions; eps goes to row jj (when jj >= M it is
   // never read) and rows beyond jj read as zero
   sts64(ea, eps);
@@ -579,12 +606,7 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
     const unsigned lim = ln.base + CAP * kRow;
     detail::Passes st;
     st.top = ln.base;
-    // the row step from the block size (every lane kernel runs kLaneThreads
-    // threads per block): ptxas cannot turn it back into an immediate, so
-    // each push's predicated advance reads it from a register instead of
-    // re-materialising the constant for every push (-70 instructions per
-    // md_mul at M = 10)
-    asm("{\n\t.reg .b32 n;\n\tmov.u32 n, %%ntid.x;\n\tshl.b32 %0, n, 3;\n\t}" : "=r"(st.step));
+    st.step = ln.step;  // see make_lane (-70 instructions per md_mul at M = 10)
     // Pass 2 runs one term behind pass 1: the pass-1 error of term i is
     // consumed by pass 2 while pass 1 processes term i+1, so the two
     // two_sums of a step are independent and interleave (ILP 2). The
@@ -666,10 +688,10 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
 #pragma unroll 1
       while (a >= ln.base && ea > elim) {
         const double n1 = lds64_at<-static_cast<int>(kRow)>(a);  // row a-1 >= spare row
-        emit_step<true>(eps, n0, ea);
+        emit_step<true>(eps, n0, ea, ln.step);
         if (a < base1) break;
         n0 = lds64_at<-2 * static_cast<int>(kRow)>(a);  // row a-2 >= spare row (a-1 >= base)
-        emit_step<true>(eps, n1, ea);
+        emit_step<true>(eps, n1, ea, ln.step);
         a -= 2 * kRow;
       }
       // emission k sits at row top-1-k; eps goes to the next emission row

@@ -16,7 +16,7 @@
 
 using namespace pse;
 constexpr int M = 10;
-constexpr int kThreads = PSE_LANE_THREADS == 384 ? 256 : PSE_LANE_THREADS;  // chains per block (V0-V4)
+constexpr int kThreads = PSE_LANE_THREADS;  // chains per block
 constexpr int LANE_ROWS = MdTraits<M>::LANE_CONV;
 
 // exp_mul_fast with parts switchable: STAGE bit 1 = compaction, bit 2 = tighten
@@ -29,6 +29,7 @@ __device__ __forceinline__ void exp_mul_v(const double (&x)[M], const double (&y
     const unsigned lim = ln.base + CAP * kRow;
     detail::Passes st;
     st.top = ln.base;
+    st.step = ln.step;
     int fed = 0, pushes = 0;
     double e1p = 0.0;
     auto feed = [&](double t) {
@@ -85,10 +86,10 @@ __device__ __forceinline__ void exp_mul_v(const double (&x)[M], const double (&y
 #pragma unroll 1
       while (a >= ln.base && ea != elim) {
         const double n1 = lds64_at<-static_cast<int>(kRow)>(a);
-        emit_step<true>(eps, n0, ea);
+        emit_step<true>(eps, n0, ea, ln.step);
         if (a < base1 || ea == elim) break;
         n0 = lds64_at<-2 * static_cast<int>(kRow)>(a);
-        emit_step<true>(eps, n1, ea);
+        emit_step<true>(eps, n1, ea, ln.step);
         a -= 2 * kRow;
       }
       sts64(ea, eps);
@@ -155,290 +156,6 @@ __global__ void __launch_bounds__(kThreads, 512 / kThreads) kstep(const double* 
   out[blockIdx.x * kThreads + tid] = __longlong_as_double(static_cast<long long>(ck));
 }
 
-
-// ---------------------------------------------------------------- V5: warp-specialised
-// PW producer warps (md_mul stream + compaction, pre-tighten result into a
-// two-slot hand-off buffer in their lane) and CW consumer warps (tighten +
-// md_add into accumulators in their own lane), paired through mbarriers.
-// Consumer warp c serves producer warps c, c+CW, ... (same SM sub-partition).
-__device__ __forceinline__ void mbar_init(unsigned a, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(unsigned a) {
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-
-// out = acc + y with the accumulator at lane rows ACC..ACC+M-1 (NaN sentinel at ACC+M)
-template <int ACC>
-__device__ __forceinline__ void acc_add_at(const double (&y)[M], double (&out)[M], Lane ln) {
-  static_for<M>([&](auto q) { sts64_at<(M + decltype(q)::value) * kRow>(ln.base, y[decltype(q)::value]); });
-  sts64_at<2 * M * kRow>(ln.base, 0.0);
-  const double xh = lds64_at<ACC * kRow>(ln.base);
-  exp_add_core<M, false, ACC, M>(xh, 0.0, y[0], 0.0, out, ln);
-  static_for<M>([&](auto q) { sts64_at<(ACC + decltype(q)::value) * kRow>(ln.base, out[decltype(q)::value]); });
-}
-
-template <class F>
-float time_kernel(F launch, int reps);
-constexpr int kPW = 8;
-constexpr int kProdRows = 1 + (MdTraits<M>::LANE - 1) + 2 * M;  // spare + stack + 2 hand-off slots
-constexpr int kHB = MdTraits<M>::LANE - 1;                       // first hand-off row (lane-relative)
-template <int J>
-__host__ __device__ constexpr int cons_rows() { return 1 + 2 * M + 1 + J * (M + 1); }  // spare + scratch + J accumulators
-template <int j>
-__host__ __device__ constexpr int acc_row() { return 2 * M + 1 + j * (M + 1); }
-
-#if PSE_LANE_THREADS == 256
-template <int CW>
-__global__ void __launch_bounds__((kPW + CW) * 32, 1) kspec(const double* __restrict__ X, const double* __restrict__ Y,
-                                                           double* out, int T, int S) {
-  static_assert(kPW * 32 == kLaneThreads, "lane pitch = producer threads");
-  constexpr int J = kPW / CW;  // producer warps per consumer warp
-  extern __shared__ double smem[];
-  __shared__ unsigned long long bars[kPW][2][2];  // [warp][slot][full, empty]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < kPW * 2) {
-    mbar_init(static_cast<unsigned>(__cvta_generic_to_shared(&bars[threadIdx.x >> 1][threadIdx.x & 1][0])), 32);
-    mbar_init(static_cast<unsigned>(__cvta_generic_to_shared(&bars[threadIdx.x >> 1][threadIdx.x & 1][1])), 32);
-  }
-  __syncthreads();
-  const double* Yb = Y + static_cast<size_t>(blockIdx.x % 8) * M * S;
-  if (warp < kPW) {
-    const int tid = threadIdx.x;  // producer thread = chain
-    Lane ln = make_lane(smem);
-#pragma unroll 1
-    for (int i = 0; i < T; ++i) {
-      double xr[M], yr[M], p[M];
-#pragma unroll
-      for (int q = 0; q < M; ++q) {
-        xr[q] = __ldg(X + q * S + i);
-        yr[q] = __ldg(Yb + q * S + tid + T - 1 - i);
-      }
-      exp_mul_v<1>(xr, yr, p, ln);
-      const int slot = i & 1;
-      const unsigned fb = static_cast<unsigned>(__cvta_generic_to_shared(&bars[warp][slot][0]));
-      if (i >= 2) mbar_wait(fb + 8, ((i >> 1) - 1) & 1);
-      const unsigned hb = ln.base + (kHB + slot * M) * kRow;
-      static_for<M>([&](auto q) { sts64_at<decltype(q)::value * kRow>(hb, p[decltype(q)::value]); });
-      mbar_arrive(fb);
-    }
-  } else {
-    const int cw = warp - kPW;
-    // consumer lane: its own rows after the producer region, same pitch
-    Lane cl{static_cast<unsigned>(__cvta_generic_to_shared(smem + (kProdRows + 1) * kLaneThreads + cw * 32 + lane))};
-    static_for<J>([&](auto jc) {
-      sts64_at<(acc_row<decltype(jc)::value>() + M) * kRow>(cl.base, __longlong_as_double(0x7ff8000000000000ll));
-    });
-    double o[J][M];
-#pragma unroll 1
-    for (int i = 0; i < T; ++i) {
-      const int slot = i & 1;
-      static_for<J>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
-        const int pw = cw + j * CW;
-        const unsigned fb = static_cast<unsigned>(__cvta_generic_to_shared(&bars[pw][slot][0]));
-        mbar_wait(fb, (i >> 1) & 1);
-        const unsigned hb = static_cast<unsigned>(__cvta_generic_to_shared(smem + kLaneThreads + pw * 32 + lane)) +
-                            (kHB + slot * M) * kRow;
-        double p[M];
-        static_for<M>([&](auto q) { p[decltype(q)::value] = lds64_at<decltype(q)::value * kRow>(hb); });
-        mbar_arrive(fb + 8);
-        tighten_fast<M, true>(p);
-        if (i == 0) {
-#pragma unroll
-          for (int q = 0; q < M; ++q) o[j][q] = p[q];
-          static_for<M>([&](auto q) { sts64_at<(acc_row<j>() + decltype(q)::value) * kRow>(cl.base, p[decltype(q)::value]); });
-        } else {
-          acc_add_at<acc_row<j>()>(p, o[j], cl);
-        }
-      });
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      unsigned long long ck = 0;
-#pragma unroll
-      for (int q = 0; q < M; ++q) ck ^= static_cast<unsigned long long>(__double_as_longlong(o[j][q])) * (q + 1);
-      out[blockIdx.x * kThreads + (cw + j * CW) * 32 + lane] = __longlong_as_double(static_cast<long long>(ck));
-    }
-  }
-}
-
-#endif
-
-// ---------------------------------------------------------------- V6: 12 producers + 4 consumers
-// One consumer warp per SM sub-partition serves the 3 producer warps there;
-// a single hand-off slot per producer (the producer only needs it free again
-// at the end of its next md_mul). Consumer lanes have their own row pitch.
-template <unsigned PITCH, bool DOWN>
-__device__ __forceinline__ void emit_step_p(double& eps, double v, unsigned& ea) {
-  double r, tt;
-  fast_two_sum(eps, v, r, tt);
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t.reg .b32 lo, hi, t;\n\t"
-      "mov.b64 {lo, hi}, %3;\n\t"
-      "and.b32 t, hi, 0x7fffffff;\n\t"
-      "or.b32 t, t, lo;\n\t"
-      "setp.ne.u32 p, t, 0;\n\t"
-      "@p st.shared.f64 [%1], %2;\n\t"
-      "@p add.u32 %1, %1, %4;\n\t"
-      "selp.f64 %0, %3, %2, p;\n\t}"
-      : "=d"(eps), "+r"(ea)
-      : "d"(r), "d"(tt), "n"(DOWN ? 0u - PITCH : PITCH));
-}
-template <unsigned PITCH, int OFF, unsigned THR>
-__device__ __forceinline__ double lds_if_p(unsigned base, unsigned lim) {
-  double v;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ge.u32 p, %2, %3;\n\tmov.b64 %0, 0;\n\t@p ld.shared.f64 %0, [%1+%4];\n\t}"
-      : "=d"(v) : "r"(base), "r"(lim), "n"(THR), "n"(OFF));
-  return v;
-}
-// acc += y with the accumulator at rows ACC.. (NaN sentinel at ACC+M), pitch PITCH
-template <unsigned PITCH, int ACC>
-__device__ __forceinline__ void acc_add_p(const double (&y)[M], double (&out)[M], unsigned base) {
-  static_for<M>([&](auto q) { sts64_at<(M + decltype(q)::value) * PITCH>(base, y[decltype(q)::value]); });
-  sts64_at<2 * M * PITCH>(base, 0.0);
-  double xh = lds64_at<ACC * PITCH>(base), yh = y[0];
-  double t[2 * M];
-  unsigned xa = base + (ACC + 1) * PITCH, ya = base + (M + 1) * PITCH;
-#pragma unroll
-  for (int p = 0; p < 2 * M; ++p) {
-    const bool take_x = fabs(xh) >= fabs(yh);
-    t[p] = take_x ? xh : yh;
-    if (p + 1 < 2 * M) {
-      const double v = lds64(take_x ? xa : ya);
-      xh = take_x ? v : xh;
-      yh = take_x ? yh : v;
-      xa += take_x ? PITCH : 0u;
-      ya += take_x ? 0u : PITCH;
-    }
-  }
-  double s = t[2 * M - 1];
-#pragma unroll
-  for (int q = 2 * M - 2; q >= 0; --q) {
-    double e;
-    two_sum(t[q], s, s, e);
-    t[q + 1] = e;
-  }
-  t[0] = s;
-  unsigned ea = base;
-  double eps = t[0];
-#pragma unroll
-  for (int q = 1; q < 2 * M; ++q) emit_step_p<PITCH, false>(eps, t[q], ea);
-  sts64(ea, eps);
-  const unsigned jb = ea - base;
-  static_for<M>([&](auto qc) {
-    constexpr int q = decltype(qc)::value;
-    out[q] = lds_if_p<PITCH, q * PITCH, q * PITCH>(base, jb);
-  });
-  tighten_fast<M, true>(out);
-  static_for<M>([&](auto q) { sts64_at<(ACC + decltype(q)::value) * PITCH>(base, out[decltype(q)::value]); });
-}
-
-constexpr int kPW6 = 12, kCW6 = 4;
-constexpr int kProd6Rows = 1 + (MdTraits<M>::LANE - 1) + M;  // spare + stack + 1 hand-off slot
-constexpr unsigned kCPitch = kCW6 * 32 * 8;
-constexpr int kCons6Rows = 1 + 2 * M + 1 + 3 * (M + 1);
-
-#if PSE_LANE_THREADS == 384
-__global__ void __launch_bounds__((kPW6 + kCW6) * 32, 1) kspec6(const double* __restrict__ X, const double* __restrict__ Y,
-                                                              double* out, int T, int S) {
-  static_assert(kPW6 * 32 == kLaneThreads, "lane pitch = producer threads");
-  constexpr int J = kPW6 / kCW6;
-  extern __shared__ double smem[];
-  __shared__ unsigned long long bars[kPW6][2];  // [warp][full, empty]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < kPW6) {
-    mbar_init(static_cast<unsigned>(__cvta_generic_to_shared(&bars[threadIdx.x][0])), 32);
-    mbar_init(static_cast<unsigned>(__cvta_generic_to_shared(&bars[threadIdx.x][1])), 32);
-  }
-  __syncthreads();
-  const double* Yb = Y + static_cast<size_t>(blockIdx.x % 8) * M * S;
-  if (warp < kPW6) {
-    const int tid = threadIdx.x;
-    Lane ln = make_lane(smem);
-    const unsigned fb = static_cast<unsigned>(__cvta_generic_to_shared(&bars[warp][0]));
-#pragma unroll 1
-    for (int i = 0; i < T; ++i) {
-      double xr[M], yr[M], p[M];
-#pragma unroll
-      for (int q = 0; q < M; ++q) {
-        xr[q] = __ldg(X + q * S + i);
-        yr[q] = __ldg(Yb + q * S + tid + T - 1 - i);
-      }
-      exp_mul_v<1>(xr, yr, p, ln);
-      if (i >= 1) mbar_wait(fb + 8, (i - 1) & 1);
-      const unsigned hb = ln.base + kHB * kRow;
-      static_for<M>([&](auto q) { sts64_at<decltype(q)::value * kRow>(hb, p[decltype(q)::value]); });
-      mbar_arrive(fb);
-    }
-  } else {
-    const int cw = warp - kPW6;
-    const unsigned cbase = static_cast<unsigned>(__cvta_generic_to_shared(smem + (kProd6Rows + 1) * kLaneThreads)) +
-                           (cw * 32 + lane) * 8 + kCPitch;  // consumer row -1 is a spare
-    static_for<J>([&](auto jc) {
-      sts64_at<(acc_row<decltype(jc)::value>() + M) * kCPitch>(cbase, __longlong_as_double(0x7ff8000000000000ll));
-    });
-    double o[J][M];
-#pragma unroll 1
-    for (int i = 0; i < T; ++i) {
-      static_for<J>([&](auto jc) {
-        constexpr int j = decltype(jc)::value;
-        const int pw = cw + j * kCW6;
-        const unsigned fb = static_cast<unsigned>(__cvta_generic_to_shared(&bars[pw][0]));
-        mbar_wait(fb, i & 1);
-        const unsigned hb = static_cast<unsigned>(__cvta_generic_to_shared(smem + kLaneThreads + pw * 32 + lane)) +
-                            kHB * kRow;
-        double p[M];
-        static_for<M>([&](auto q) { p[decltype(q)::value] = lds64_at<decltype(q)::value * kRow>(hb); });
-        mbar_arrive(fb + 8);
-        tighten_fast<M, true>(p);
-        if (i == 0) {
-#pragma unroll
-          for (int q = 0; q < M; ++q) o[j][q] = p[q];
-          static_for<M>([&](auto q) { sts64_at<(acc_row<j>() + decltype(q)::value) * kCPitch>(cbase, p[decltype(q)::value]); });
-        } else {
-          acc_add_p<kCPitch, acc_row<j>()>(p, o[j], cbase);
-        }
-      });
-    }
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      unsigned long long ck = 0;
-#pragma unroll
-      for (int q = 0; q < M; ++q) ck ^= static_cast<unsigned long long>(__double_as_longlong(o[j][q])) * (q + 1);
-      out[blockIdx.x * (kPW6 * 32) + (cw + j * kCW6) * 32 + lane] = __longlong_as_double(static_cast<long long>(ck));
-    }
-  }
-}
-#endif
-
-#if PSE_LANE_THREADS == 256
-template <int CW>
-void run_spec(const double* X, const double* Y, double* out, int T, int S, int blocks, double peak) {
-  const size_t sh = static_cast<size_t>(kProdRows + 1 + cons_rows<kPW / CW>()) * kLaneThreads * sizeof(double);
-  cudaFuncSetAttribute(kspec<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh));
-  float ms = time_kernel([&] { kspec<CW><<<blocks, (kPW + CW) * 32, sh>>>(X, Y, out, T, S); }, 5);
-  cudaError_t e = cudaGetLastError();
-  std::vector<unsigned long long> h(blocks * kThreads);
-  cudaMemcpy(h.data(), out, h.size() * 8, cudaMemcpyDeviceToHost);
-  unsigned long long c = 0;
-  for (auto v : h) c = c * 1000003ull + v;
-  const double steps = static_cast<double>(blocks) * kThreads * T;
-  const double ops = static_cast<double>(blocks) * kThreads * (T * 1944.0 + (T - 1) * 279.0);
-  const double cyc = ms * 1.965e6 / (steps / 32.0 / (148.0 * 4));
-  printf("V5 specialised %dP+%dC             %8.3f ms  %7.1f cyc/warp-step/SMSP  alg %.2f T ops/s  frac %.3f  ck %016llx %s (smem %zu)\n",
-         kPW, CW, ms, cyc, ops / ms / 1e9, ops / ms / 1e9 / peak, c, e == cudaSuccess ? "" : cudaGetErrorString(e), sh);
-}
-#endif
 
 template <class F>
 float time_kernel(F launch, int reps) {
@@ -511,26 +228,6 @@ int main(int argc, char** argv) {
   cudaMalloc(&out, static_cast<size_t>(blocks) * kThreads * 8);
   cudaMemcpy(X, hx.data(), hx.size() * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(Y, hy.data(), hy.size() * 8, cudaMemcpyHostToDevice);
-#if PSE_LANE_THREADS == 384
-  {
-    const int blocks6 = 148 * 2 * waves;
-    const size_t sh = static_cast<size_t>(kProd6Rows + 1) * kLaneThreads * 8 + static_cast<size_t>(kCons6Rows) * kCPitch;
-    cudaFuncSetAttribute(kspec6, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh));
-    double* out6;
-    cudaMalloc(&out6, static_cast<size_t>(blocks6) * 384 * 8);
-    float ms = time_kernel([&] { kspec6<<<blocks6, (kPW6 + kCW6) * 32, sh>>>(X, Y, out6, T, S); }, 5);
-    cudaError_t e = cudaGetLastError();
-    const double steps = static_cast<double>(blocks6) * 384 * T;
-    const double ops = static_cast<double>(blocks6) * 384 * (T * 1944.0 + (T - 1) * 279.0);
-    const double cyc = ms * 1.965e6 / (steps / 32.0 / (148.0 * 4));
-    std::vector<unsigned long long> h(static_cast<size_t>(blocks6) * 384);
-    cudaMemcpy(h.data(), out6, h.size() * 8, cudaMemcpyDeviceToHost);
-    unsigned long long c = 0;
-    for (size_t k = 0; k < h.size(); k += 7) c += h[k];
-    printf("V6 specialised 12P+4C             %8.3f ms  %7.1f cyc/warp-step/SMSP  alg %.2f T ops/s  frac %.3f  sum %016llx %s (smem %zu)\n",
-           ms, cyc, ops / ms / 1e9, ops / ms / 1e9 / peak, c, e == cudaSuccess ? "" : cudaGetErrorString(e), sh);
-  }
-#else
   printf("T=%d steps, %d blocks of %d threads, lane %d rows\n", T, blocks, kThreads, LANE_ROWS);
   run<0>("production mul+add", X, Y, out, T, S, blocks, peak);
   if (argc > 3) return 0;  // V0 only
@@ -538,10 +235,5 @@ int main(int argc, char** argv) {
   run<2>("mul stream only", X, Y, out, T, S, blocks, peak);
   run<3>("mul, no tighten", X, Y, out, T, S, blocks, peak);
   run<4>("add only", X, Y, out, T, S, blocks, peak);
-#if PSE_LANE_THREADS == 256
-  run_spec<4>(X, Y, out, T, S, blocks, peak);
-  run_spec<8>(X, Y, out, T, S, blocks, peak);
-#endif
-#endif
   return 0;
 }
