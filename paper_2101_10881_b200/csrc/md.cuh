@@ -682,11 +682,15 @@ __device__ __forceinline__ void exp_mul_fast(const double (&x)[M], const double 
       double eps = st.s2;
       unsigned a = st.top - kRow;        // row of the next term to pop
       unsigned ea = st.top - kRow;       // row of the next emission
-      const unsigned elim = st.top - (M + 1) * kRow;  // ea <= elim <=> M emitted
+      // ea <= elim <=> M emitted. Signed: with fewer than M+1 terms on the
+      // stack elim lies below the lane and, near the bottom of the shared
+      // window, below address 0 (as an unsigned bound it wrapped, and the
+      // loop popped nothing: x*1 lost every limb but the first).
+      const int elim = static_cast<int>(st.top) - (M + 1) * static_cast<int>(kRow);
       const unsigned base1 = ln.base + kRow;
       double n0 = lds64(a);
 #pragma unroll 1
-      while (a >= ln.base && ea > elim) {
+      while (a >= ln.base && static_cast<int>(ea) > elim) {
         const double n1 = lds64_at<-static_cast<int>(kRow)>(a);  // row a-1 >= spare row
         emit_step<true>(eps, n0, ea, ln.step);
         if (a < base1) break;
