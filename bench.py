@@ -304,6 +304,7 @@ CONV_KERNEL = {
     "dataflow": "k_conv_flow<{m},real> (one persistent launch per evaluation wave)",
     "hybrid": "k_conv<{m},real> for the large conv layers, then k_conv_flow<{m},real> for the trailing small ones",
     "cta": "k_conv_cta<{m},real> (one block per independent job group and point, CTA-local dataflow)",
+    "cta_layers": "k_conv_ctl<{m},real> (one block per independent job group and point, its layers in order)",
 }
 
 

@@ -220,8 +220,17 @@ int pse_plan_stream(const pse_plan* p, void** stream);
  * PSE_CONV_DATAFLOW (the same tasks in one persistent launch) or
  * PSE_CONV_HYBRID (layered for the large layers, then one dataflow launch
  * for the trailing small ones) or PSE_CONV_CTA (one block per independent job
- * group and point, the group's band tasks synchronised in shared memory) */
-enum { PSE_CONV_LAYERED = 1, PSE_CONV_WAVES = 2, PSE_CONV_DATAFLOW = 3, PSE_CONV_HYBRID = 4, PSE_CONV_CTA = 5 };
+ * group and point, the group's band tasks synchronised in shared memory) or
+ * PSE_CONV_CTA_LAYERS (one block per independent job group and point, the
+ * group's conv layers in order with a block barrier between them) */
+enum {
+  PSE_CONV_LAYERED = 1,
+  PSE_CONV_WAVES = 2,
+  PSE_CONV_DATAFLOW = 3,
+  PSE_CONV_HYBRID = 4,
+  PSE_CONV_CTA = 5,
+  PSE_CONV_CTA_LAYERS = 6
+};
 int pse_plan_conv_path(const pse_plan* p, int32_t batch, int32_t* path);
 /* host only (no device): the banded task schedule of a whole graph with band
  * width W (16 or 32), in dataflow order (flow != 0) or waves of `procs` warps;

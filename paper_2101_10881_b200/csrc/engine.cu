@@ -559,7 +559,7 @@ struct Plan {
   bool banded(int batch) const { return band_first(batch) < static_cast<int>(layer_rows.size()); }
 
   // the global dataflow kernel (also the CTA path's fallback)
-  bool flow() const { return conv_mode == 3 || conv_mode == 0 || conv_mode == 4; }
+  bool flow() const { return conv_mode == 3 || conv_mode == 0 || conv_mode == 4 || conv_mode == 5; }
 
   // ---- CTA-local dataflow (CtaArgs in kernels.cuh): one block per
   // independent job group (connected component of the dynamic slots: whole
@@ -574,6 +574,15 @@ struct Plan {
     int4 *jobs = nullptr, *tasks = nullptr;
     int *group_off = nullptr, *dep_off = nullptr, *deps = nullptr;
     double makespan = 0;  // simulated, in steps: the slowest group
+    // layered form (k_conv_ctl): the group's layers in order, a block barrier
+    // between them -- the M = 1 default (see prefer_cta) and PSE_CONV_MODE=ctl
+    bool layered = false;
+    int4* ljobs = nullptr;
+    int *layer_off = nullptr, *lgroup_off = nullptr;
+    int *stage_off = nullptr, *stage_slot = nullptr, *gjob_off = nullptr;  // see CtlArgs
+    int4* sidx = nullptr;
+    int max_stage = 0;
+    size_t table_bytes = 0;
   } cta;
 
   // The CTA-local path is taken when forced (PSE_CONV_MODE=cta) and, by
@@ -583,10 +592,22 @@ struct Plan {
   // kernel's per-task L2 round trips dominate (C3 / C3' m=1: 0.92 / 1.16 ->
   // 0.39 ms). Many small groups (p1, p3) stay on the global kernel (C2 m=1:
   // 0.22 vs 0.61 ms CTA-local); at M >= 2 the global kernel is faster.
+  //
+  // At M = 1 the default is the layered form (k_conv_ctl): a step is one
+  // DMUL + DADD, so even a layer-by-layer walk of p2's 64 layers is short
+  // next to the band tasks' hand-out and flag costs (C3 m=1: see DESIGN).
   bool prefer_cta() const {
-    return conv_mode == 4 ||
+    return conv_mode == 4 || conv_mode == 5 ||
            (conv_mode == 0 && m == 1 && ncomps > 0 && ncomps <= 2 * sms && nrows_mine >= int64_t(32) * ncomps);
   }
+  static int ctl_dbg() {
+    static const int v = [] {
+      const char* e = getenv("PSE_CTL_DBG");
+      return e ? atoi(e) : 0;
+    }();
+    return v;
+  }
+  bool cta_layered() const { return conv_mode == 5 || (conv_mode == 0 && m == 1); }
   bool cta_mode() const { return prefer_cta() && cta_ready(); }
   bool cta_ready() const { return cta.built && cta.ok; }
 
@@ -604,6 +625,81 @@ struct Plan {
         rows[layer_comp[L2][r]].push_back(layer_rows[L2][r]);
         rlayer[layer_comp[L2][r]].push_back(static_cast<int>(L2));
       }
+    if (cta_layered()) {
+      // jobs of each group layer by layer: (in1, in2, out, copy | layer << 8);
+      // per (group, layer) the distinct input slots (M = 1 stages them in
+      // shared memory), each job's staged (in1, in2) and the index of its
+      // output in the next layer's list (-1: not read there)
+      std::vector<int4> lj, si;
+      std::vector<int> loff(1, 0), lgoff(1, 0), soff(1, 0), sslot, gjoff(1, 0);
+      size_t table_bytes = 0;
+      for (int c = 0; c < ncomps; ++c) {
+        const size_t j_first = lj.size(), s_first = sslot.size(), l_first = loff.size() - 1;
+        // layer boundaries of the group's rows
+        std::vector<size_t> lb;
+        for (size_t t = 0; t < rows[c].size(); ++t)
+          if (t == 0 || rlayer[c][t] != rlayer[c][t - 1]) lb.push_back(t);
+        lb.push_back(rows[c].size());
+        std::vector<std::map<int64_t, int>> lists(lb.size() - 1);
+        for (size_t q = 0; q + 1 < lb.size(); ++q) {
+          std::map<int64_t, int>& st = lists[q];
+          auto stage = [&](int64_t slot) {
+            auto it = st.find(slot);
+            if (it != st.end()) return it->second;
+            const int e = static_cast<int>(st.size());
+            st[slot] = e;
+            return e;
+          };
+          std::set<int64_t> prev_out;
+          if (q > 0)
+            for (size_t t = lb[q - 1]; t < lb[q]; ++t) prev_out.insert(rows[c][t].out);
+          std::vector<int64_t> order;
+          for (size_t t = lb[q]; t < lb[q + 1]; ++t) {
+            const ConvRow& r = rows[c][t];
+            const size_t before = st.size();
+            const int sx = stage(r.in1);
+            if (st.size() > before) order.push_back(r.in1);
+            int sy = sx;
+            if (!r.copy) {
+              const size_t b2 = st.size();
+              sy = stage(r.in2);
+              if (st.size() > b2) order.push_back(r.in2);
+            }
+            lj.push_back(make_int4(static_cast<int>(r.in1), static_cast<int>(r.in2), static_cast<int>(r.out),
+                                   (r.copy ? 1 : 0) | (rlayer[c][t] << 8)));
+            si.push_back(make_int4(sx, sy, -1, 0));
+          }
+          for (int64_t slot : order) sslot.push_back(static_cast<int>(slot * 2 + (prev_out.count(slot) ? 1 : 0)));
+          loff.push_back(static_cast<int>(lj.size()));
+          soff.push_back(static_cast<int>(sslot.size()));
+          cta.max_stage = std::max(cta.max_stage, static_cast<int>(st.size()));
+        }
+        // outputs read by the next layer of the group
+        for (size_t q = 0; q + 2 < lb.size(); ++q)
+          for (size_t t = lb[q]; t < lb[q + 1]; ++t) {
+            auto it = lists[q + 1].find(rows[c][t].out);
+            if (it != lists[q + 1].end()) si[j_first + t].z = it->second;
+          }
+        lgoff.push_back(static_cast<int>(loff.size()) - 1);
+        gjoff.push_back(static_cast<int>(lj.size()));
+        const size_t nj = lj.size() - j_first, nl = loff.size() - 1 - l_first, ns = sslot.size() - s_first;
+        table_bytes = std::max(table_bytes, nj * 2 * sizeof(int4) + 2 * (nl + 1) * sizeof(int) + ns * sizeof(int));
+      }
+      if (!L->ctl_fits(cta.max_stage, d, table_bytes)) return;  // stays on the global dataflow path
+      cta.table_bytes = table_bytes;
+      cta.ngroups = ncomps;
+      cta.ljobs = dev_upload(lj, stream);
+      cta.layer_off = dev_upload(loff, stream);
+      cta.lgroup_off = dev_upload(lgoff, stream);
+      cta.stage_off = dev_upload(soff, stream);
+      cta.stage_slot = dev_upload(sslot.empty() ? std::vector<int>{0} : sslot, stream);
+      cta.sidx = dev_upload(si, stream);
+      cta.gjob_off = dev_upload(gjoff, stream);
+      ck(cudaStreamSynchronize(stream), "ctl upload");
+      cta.layered = true;
+      cta.ok = true;
+      return;
+    }
     const int warps = L->threads / 32;
     const Costs cst = costs(m);
     // fixed cost of a task (shared-memory hand-out and flags) in steps
@@ -741,6 +837,13 @@ struct Plan {
     cudaFree(cta.group_off);
     cudaFree(cta.dep_off);
     cudaFree(cta.deps);
+    cudaFree(cta.ljobs);
+    cudaFree(cta.layer_off);
+    cudaFree(cta.lgroup_off);
+    cudaFree(cta.stage_off);
+    cudaFree(cta.stage_slot);
+    cudaFree(cta.sidx);
+    cudaFree(cta.gjob_off);
     cudaFree(stamps);
     cudaFree(peer_list);
     cudaFree(peer_first);
@@ -828,7 +931,12 @@ struct Plan {
         }
       }
     }
-    if (first < static_cast<int>(layer_rows.size()) && cta_mode()) {  // CTA-local dataflow
+    if (first < static_cast<int>(layer_rows.size()) && cta_mode() && cta.layered) {  // CTA-local layers
+      CtlArgs a{arena,         G,          cta.ljobs, cta.layer_off,  cta.lgroup_off, cta.ngroups, batch, (d + 2) / 2,
+                stamps,        cta.stage_off, cta.stage_slot, cta.sidx, cta.gjob_off, cta.max_stage, ctl_dbg()};
+      L->conv_ctl(a, cta.table_bytes, stream);
+      ++launches;
+    } else if (first < static_cast<int>(layer_rows.size()) && cta_mode()) {  // CTA-local dataflow
       CtaArgs a{arena, G, cta.jobs, cta.tasks, cta.group_off, cta.dep_off, cta.deps, cta.ngroups, batch, cta.W, stamps};
       if (!L->conv_cta(a, cta.max_units, stream)) throw std::logic_error("CTA-local dataflow does not fit");
       ++launches;
@@ -1107,7 +1215,7 @@ Plan* build_plan(const pse_graph_desc& g, int device, int max_batch, const std::
     {
       const char* cm = getenv("PSE_CONV_MODE");
       const std::string m = cm ? cm : "";
-      p->conv_mode = m == "layer" ? 1 : m == "band" ? 2 : m == "flow" ? 3 : m == "cta" ? 4 : 0;
+      p->conv_mode = m == "layer" ? 1 : m == "band" ? 2 : m == "flow" ? 3 : m == "cta" ? 4 : m == "ctl" ? 5 : 0;
       const char* br = getenv("PSE_BAND_ROUNDS");
       if (br && atof(br) > 0) p->band_rounds = atof(br);
       const char* fs = getenv("PSE_FLOW_SLACK");
@@ -1662,7 +1770,7 @@ int pse_plan_conv_path(const pse_plan* p, int32_t batch, int32_t* path) {
   if (!p || !path || batch < 1 || batch > p->p->max_batch) return PSE_EINVAL;
   const pse::Plan& P = *p->p;
   *path = !P.banded(batch)          ? PSE_CONV_LAYERED
-          : P.cta_mode()            ? PSE_CONV_CTA
+          : P.cta_mode()            ? (P.cta.layered ? PSE_CONV_CTA_LAYERS : PSE_CONV_CTA)
           : !P.flow()               ? PSE_CONV_WAVES
           : P.band_first(batch) > 0 ? PSE_CONV_HYBRID
                                     : PSE_CONV_DATAFLOW;

@@ -191,6 +191,39 @@ struct CtaArgs {
   Stamp* stamps;         // as BandArgs
 };
 
+// CTA-local layered convolution (deep graphs of few large job groups at small
+// precisions): ONE block per independent job group and point runs the
+// group's conv layers in order, a block barrier between layers; within a
+// layer every thread takes whole coefficient pairs (k, d-k) of the layer's
+// jobs, as k_conv does. The operands were written earlier in the launch by
+// this block (or staged before it), so they are read through L1. A layer's
+// critical path is one pair's d+2 steps; at M = 1 a step is one DMUL + DADD,
+// so the 64 layers of p2 cost ~64 x (d+2) dependent DADDs -- no task
+// hand-out, no completion flags.
+struct CtlArgs {
+  double* arena;
+  Geom G;
+  const int4* jobs;       // (in1, in2, out, copy | graph conv layer << 8), groups' layers one after another
+  const int* layer_off;   // [nlayers+1] first job of each (group, layer)
+  const int* group_off;   // [ngroups+1] first (group, layer) of each group
+  int ngroups;
+  int batch;
+  int npairs;             // (d+2)/2
+  Stamp* stamps;          // as BandArgs
+  // M = 1 (real): each (group, layer)'s input series live in shared memory.
+  // The group's job table and lists are copied to shared memory once; the
+  // next layer's inputs are prefetched (cp.async) while a layer computes,
+  // except those the layer itself produces, which its chains write straight
+  // into the next layer's buffer as well as to the arena. stage_slot entries
+  // are slot * 2 + (1 if produced by the previous layer).
+  const int* stage_off;   // [nlayers+1] first entry of each (group, layer)'s list
+  const int* stage_slot;
+  const int4* sidx;       // per job: staged (in1, in2) in its layer's list, its out in the next layer's (or -1)
+  const int* gjob_off;    // [ngroups+1] first job of each group
+  int max_stage;          // longest list
+  int dbg;                // timing experiments only (PSE_CTL_DBG): 1 skips the chains, 2 the prefetch
+};
+
 struct Launchers {
   void (*conv)(const ConvArgs&, cudaStream_t);
   void (*conv_band)(const BandArgs&, cudaStream_t);
@@ -200,6 +233,8 @@ struct Launchers {
   // completion flags do not fit next to the lanes in shared memory
   bool (*conv_cta)(const CtaArgs&, int max_units, cudaStream_t);
   bool (*cta_fits)(int max_units);
+  void (*conv_ctl)(const CtlArgs&, size_t table_bytes, cudaStream_t);
+  bool (*ctl_fits)(int max_stage, int d, size_t table_bytes);
   void (*conv_prod)(const SplitArgs&, cudaStream_t);
   void (*conv_accum)(const SplitArgs&, cudaStream_t);
   void (*add)(const AddArgs&, cudaStream_t);
@@ -293,22 +328,37 @@ constexpr int conv_default_minb() {
   return 4;
 }
 
-template <int M, bool CPLX>
-__device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm) {
-  const int pair = static_cast<int>(g % a.npairs);
-  const int64_t r = g / a.npairs;
-  const int jb = static_cast<int>(r % a.njobs);
-  const int64_t pt = r / a.njobs;
-  const int4 J = a.jobs[jb];
-  const int S = a.G.S, d = a.G.d;
-  double* base = a.arena + pt * a.G.point_words;
-  const double* __restrict__ X = base + static_cast<int64_t>(J.x) * a.G.slot_words;
-  const double* __restrict__ Y = base + static_cast<int64_t>(J.y) * a.G.slot_words;
-  double* Z = base + static_cast<int64_t>(J.z) * a.G.slot_words;
+// operand loads of a coefficient-pair chain: the read-only path, or (COH:
+// the operand may have been written earlier in the same launch by this
+// block) L1-cached coherent loads
+template <bool COH>
+__device__ __forceinline__ double ld_op(const double* p) {
+  if constexpr (COH)
+    return __ldca(p);
+  else
+    return __ldg(p);
+}
+template <int M, bool COH>
+__device__ __forceinline__ void load_md_op(const double* __restrict__ src, int S, int j, double (&v)[M]) {
+  const double* p = src + j;
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    v[q] = ld_op<COH>(p);
+    p += S;
+  }
+}
+
+// the chains of coefficient pair `pair` of job J (slots of one point at base)
+template <int M, bool CPLX, bool COH>
+__device__ __forceinline__ void conv_pair_at(const int4 J, double* base, const Geom& G, int pair, Lane sm) {
+  const int S = G.S, d = G.d;
+  const double* __restrict__ X = base + static_cast<int64_t>(J.x) * G.slot_words;
+  const double* __restrict__ Y = base + static_cast<int64_t>(J.y) * G.slot_words;
+  double* Z = base + static_cast<int64_t>(J.z) * G.slot_words;
   const int k1 = pair, k2 = d - pair;
   constexpr int Q = CPLX ? 2 * M : M;
 
-  if (J.w) {  // copy job (executor.cpp:130-133): out := in1
+  if (J.w & 1) {  // copy job (executor.cpp:130-133): out := in1
 #pragma unroll 1
     for (int q = 0; q < Q; ++q) {
       Z[q * S + k1] = X[q * S + k1];
@@ -327,7 +377,7 @@ __device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm)
       const bool second = t >= n1;
       const int kk = second ? k2 : k1;
       const int i = second ? t - n1 : t;
-      const double p = __dmul_rn(__ldg(X + i), __ldg(Y + kk - i));
+      const double p = __dmul_rn(ld_op<COH>(X + i), ld_op<COH>(Y + kk - i));
       acc = i == 0 ? p : __dadd_rn(acc, p);
       if (i == kk) Z[kk] = acc;
     }
@@ -341,8 +391,8 @@ __device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm)
       const int kk = second ? k2 : k1;
       const int i = second ? t - n1 : t;
       double xr[M], yr[M], p[M], o[M];
-      load_md<M>(X, S, i, xr);
-      load_md<M>(Y, S, kk - i, yr);
+      load_md_op<M, COH>(X, S, i, xr);
+      load_md_op<M, COH>(Y, S, kk - i, yr);
       exp_mul_fast<M>(xr, yr, p, sm);
       if (i == 0) {
         copy_md<M>(o, p);
@@ -374,11 +424,11 @@ __device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm)
         const int kk = second ? k2 : k1;
         const int i = second ? t - n1 : t;
         double xa[M], yb[M], p1[M], p2[M], pr[M];
-        load_md<M>(X, S, i, xa);
-        load_md<M>(Y1, S, kk - i, yb);
+        load_md_op<M, COH>(X, S, i, xa);
+        load_md_op<M, COH>(Y1, S, kk - i, yb);
         exp_mul_fast<M>(xa, yb, p1, sm);  // xr * yr | xr * yi
-        load_md<M>(X + M * S, S, i, xa);
-        load_md<M>(Y2, S, kk - i, yb);
+        load_md_op<M, COH>(X + M * S, S, i, xa);
+        load_md_op<M, COH>(Y2, S, kk - i, yb);
         exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yi | xi * yr
         // md_sub = exp_add of the negation (expansion.hpp:160-170): flip the
         // sign bits for the real part, branch-free
@@ -413,11 +463,11 @@ __device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm)
       // (xr + i xi)(yr + i yi): pseries.cpp:50-51 operand order; each md_mul
       // loads its own operands (L1 hits) so that at most one pair is live
       double xa[M], yb[M], p1[M], p2[M], pr[M];
-      load_md<M>(X, S, i, xa);
-      load_md<M>(Y, S, kk - i, yb);
+      load_md_op<M, COH>(X, S, i, xa);
+      load_md_op<M, COH>(Y, S, kk - i, yb);
       exp_mul_fast<M>(xa, yb, p1, sm);  // xr * yr
-      load_md<M>(X + M * S, S, i, xa);
-      load_md<M>(Y + M * S, S, kk - i, yb);
+      load_md_op<M, COH>(X + M * S, S, i, xa);
+      load_md_op<M, COH>(Y + M * S, S, kk - i, yb);
       exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yi
       exp_sub_fast<M>(p1, p2, pr, sm);
       if constexpr (LANE_RE) {
@@ -433,10 +483,10 @@ __device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm)
         else exp_add_fast<M>(ar, pr, ar, sm);
         if (i == kk) store_md<M>(Z, S, kk, ar);
       }
-      load_md<M>(X, S, i, xa);
+      load_md_op<M, COH>(X, S, i, xa);
       exp_mul_fast<M>(xa, yb, p1, sm);  // xr * yi
-      load_md<M>(X + M * S, S, i, xa);
-      load_md<M>(Y, S, kk - i, yb);
+      load_md_op<M, COH>(X + M * S, S, i, xa);
+      load_md_op<M, COH>(Y, S, kk - i, yb);
       exp_mul_fast<M>(xa, yb, p2, sm);  // xi * yr
       exp_add_fast<M>(p1, p2, pr, sm);
       if constexpr (LANE_RE) {
@@ -457,6 +507,15 @@ __device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm)
       }
     }
   }
+}
+
+template <int M, bool CPLX>
+__device__ __forceinline__ void conv_pair(const ConvArgs& a, int64_t g, Lane sm) {
+  const int pair = static_cast<int>(g % a.npairs);
+  const int64_t r = g / a.npairs;
+  const int jb = static_cast<int>(r % a.njobs);
+  const int64_t pt = r / a.njobs;
+  conv_pair_at<M, CPLX, false>(a.jobs[jb], a.arena + pt * a.G.point_words, a.G, pair, sm);
 }
 
 template <int M, bool CPLX, int MINB>
@@ -919,6 +978,243 @@ __global__ void __launch_bounds__(kConvThreads, 1) k_conv_cta(const CtaArgs a) {
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// M = 1 chains in register blocks. A job's d+1 chains z_k = sum_i x_i y_{k-i}
+// (ascending i, pseries.cpp:41-48) are cut into blocks of kCtlR = 2 adjacent
+// chains k0, k0+1 (k0 = 2b, B = ceil((d+1)/2) blocks); thread q of a job
+// runs block nB = B-1-q and, when distinct, block nA = q side by side, one
+// step of each per step s: the chains of both blocks need x_s, chain r of a
+// block needs y_{k0+r-s} -- the element chain r-1 used one step earlier --
+// so a step is one x load, two y loads and four independent DMUL + DADD
+// pairs. The loop runs block B's chunks (2 steps each); block A's chains end
+// inside it (chain r after step 2nA + r), where their sums are copied out
+// (predicated), and then run on over padding words that nothing stores. An
+// accumulator starts at -0 (x + -0 == x bitwise for every x, so the first
+// sum is the first product, as in the reference).
+//
+// Staged series are stored transposed by two -- element j at (j % 2) *
+// kCtlLS + kCtlOff + j / 2 -- so that the y loads of the lanes of a warp
+// (consecutive q of one job) hit consecutive words (x_s is a broadcast), with
+// kCtlOff words of padding in front of each half for block A's overrun.
+constexpr int kCtlR = 2;
+constexpr int kCtlLS = 256;  // half-series stride: d + 1 <= 256
+constexpr int kCtlOff = 128;
+__host__ __device__ constexpr int ctl_series_words() { return kCtlR * kCtlLS; }
+__device__ __forceinline__ int ctl_pos(int j) { return (j & 1) * kCtlLS + kCtlOff + (j >> 1); }
+
+// thread q's chains of one job (X, Y staged; Z the arena series; W the next
+// layer's staged copy of Z or null). The operands of chunk u+1 are loaded
+// before chunk u computes (a warp issues in order: a load placed after the
+// chunk's sums would put the load -> DMUL -> DADD latency on every chunk);
+// chunks go in pairs so the two operand sets swap roles without copies.
+__device__ __forceinline__ void ctl_pair_m1(const double* X, const double* Y, double* Z, double* W, int q, int B, int d) {
+  constexpr int LS = kCtlLS;
+  const int nA = q, nB = B - 1 - q;
+  const bool hasA = nA < nB;
+  const double* px = X + kCtlOff;
+  const double* pa = Y + kCtlOff + nA;  // y_{2(b-u)} at pa[0], y_{2(b-u)-1} at pa[LS-1]
+  const double* pb = Y + kCtlOff + nB;
+  double a0 = -0.0, a1 = -0.0, b0 = -0.0, b1 = -0.0;  // chains k0, k0+1 of blocks A, B
+  double sa0 = 0.0, sa1 = 0.0;                       // block A's results
+  double wa1 = pa[LS], wb1 = pb[LS];                 // y_{k0+1}
+  struct Ops {
+    double x0, x1, ya0, ya1, yb0, yb1;  // x_s, x_{s+1}; y_{k0-s}, y_{k0-s-1} of A and B
+  };
+  auto load = [&](Ops& o) {
+    o.x0 = px[0];
+    o.x1 = px[LS];
+    o.ya0 = pa[0];
+    o.ya1 = pa[LS - 1];
+    o.yb0 = pb[0];
+    o.yb1 = pb[LS - 1];
+  };
+  // one chunk: steps s = 2u, 2u+1. Ring: at step s chain r uses y_{k0+r-s}.
+  auto chunk = [&](const Ops& o, int u) {
+    // s = 2u: chain 0 <- y_{k0-s} (new), chain 1 <- y_{k0+1-s} (w1)
+    a0 = __dadd_rn(a0, __dmul_rn(o.x0, o.ya0));
+    a1 = __dadd_rn(a1, __dmul_rn(o.x0, wa1));
+    b0 = __dadd_rn(b0, __dmul_rn(o.x0, o.yb0));
+    b1 = __dadd_rn(b1, __dmul_rn(o.x0, wb1));
+    const bool endA = u == nA;
+    sa0 = endA ? a0 : sa0;  // chain 2nA of block A ends at this step
+    // s = 2u+1: chain 0 <- y_{k0-s} (new), chain 1 <- y_{k0+1-s} = y_{k0-2u}
+    a1 = __dadd_rn(a1, __dmul_rn(o.x1, o.ya0));
+    a0 = __dadd_rn(a0, __dmul_rn(o.x1, o.ya1));
+    b1 = __dadd_rn(b1, __dmul_rn(o.x1, o.yb0));
+    b0 = __dadd_rn(b0, __dmul_rn(o.x1, o.yb1));
+    sa1 = endA ? a1 : sa1;
+    wa1 = o.ya1;  // y_{k0+1-(s+2)}
+    wb1 = o.yb1;
+  };
+  auto advance = [&]() {
+    ++px;
+    --pa;
+    --pb;
+  };
+  Ops o0, o1;
+  load(o0);
+  int u = 0;
+#pragma unroll 1
+  for (; u + 2 <= nB; u += 2) {
+    advance();
+    load(o1);
+    chunk(o0, u);
+    advance();
+    load(o0);
+    chunk(o1, u + 1);
+  }
+  if (u < nB) {
+    advance();
+    load(o1);
+    chunk(o0, u);
+    o0 = o1;
+    ++u;
+  }
+  // block B's last chunk (u == nB): chain 2nB ends at its first step
+  b0 = __dadd_rn(b0, __dmul_rn(o0.x0, o0.yb0));
+  b1 = __dadd_rn(b1, __dmul_rn(o0.x0, wb1));
+  b1 = __dadd_rn(b1, __dmul_rn(o0.x1, o0.yb0));
+  const int kb = 2 * nB;
+  if (kb <= d) {
+    Z[kb] = b0;
+    if (W) W[ctl_pos(kb)] = b0;
+  }
+  if (kb + 1 <= d) {
+    Z[kb + 1] = b1;
+    if (W) W[ctl_pos(kb + 1)] = b1;
+  }
+  if (hasA) {
+    const int ka = 2 * nA;
+    Z[ka] = sa0;
+    Z[ka + 1] = sa1;
+    if (W) {
+      W[ctl_pos(ka)] = sa0;
+      W[ctl_pos(ka + 1)] = sa1;
+    }
+  }
+}
+
+// M = 1, real: the group's layers with shared-memory operands (see CtlArgs)
+__device__ __forceinline__ void ctl_group_m1(const CtlArgs& a, double* smem_d, int grp, double* base) {
+  const int d = a.G.d, n1 = d + 1;
+  constexpr int SW = ctl_series_words();
+  const int B = (d + kCtlR) / kCtlR, nthr = (B + 1) / 2;  // blocks and threads per job
+  const int64_t sw = a.G.slot_words;
+  const int jb0 = a.gjob_off[grp], nj = a.gjob_off[grp + 1] - jb0;
+  const int lb0 = a.group_off[grp], nl = a.group_off[grp + 1] - lb0;
+  const int sb0 = a.stage_off[lb0], ns = a.stage_off[lb0 + nl] - sb0;
+  // shared memory: the two stage buffers, then the group's tables
+  double* buf0 = smem_d;
+  double* buf1 = smem_d + static_cast<size_t>(a.max_stage) * SW;
+  int4* sj = reinterpret_cast<int4*>(buf1 + static_cast<size_t>(a.max_stage) * SW);
+  int4* sx = sj + nj;
+  int* loff = reinterpret_cast<int*>(sx + nj);  // [nl+1], group-relative job index
+  int* soff = loff + nl + 1;                    // [nl+1], group-relative entry index
+  int* sslot = soff + nl + 1;                   // [ns]
+  for (int t = threadIdx.x; t < nj; t += blockDim.x) {
+    sj[t] = a.jobs[jb0 + t];
+    sx[t] = a.sidx[jb0 + t];
+  }
+  for (int t = threadIdx.x; t <= nl; t += blockDim.x) {
+    loff[t] = a.layer_off[lb0 + t] - jb0;
+    soff[t] = a.stage_off[lb0 + t] - sb0;
+  }
+  for (int t = threadIdx.x; t < ns; t += blockDim.x) sslot[t] = a.stage_slot[sb0 + t];
+  __syncthreads();
+  // layer 0's inputs: every entry from the arena
+  for (int w = threadIdx.x; w < (soff[1] - soff[0]) * n1; w += blockDim.x) {
+    const int e = w / n1, c = w - e * n1;
+    cp_async8(buf0 + e * SW + ctl_pos(c), base + (sslot[e] >> 1) * sw + c);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+#pragma unroll 1
+  for (int l = 0; l < nl; ++l) {
+    const double* cur = (l & 1) ? buf1 : buf0;
+    double* nxt = (l & 1) ? buf0 : buf1;
+    const int j0 = loff[l], n = (loff[l + 1] - j0) * nthr;
+    if (l + 1 < nl && !(a.dbg & 2)) {
+      // prefetch the next layer's inputs that this layer does not produce,
+      // by the threads without chains first (counted from the last thread)
+      const int e0 = soff[l + 1], nw = (soff[l + 2] - e0) * n1;
+      for (int w = blockDim.x - 1 - threadIdx.x; w < nw; w += blockDim.x) {
+        const int e = w / n1, c = w - e * n1;
+        const int ss = sslot[e0 + e];
+        if (!(ss & 1)) cp_async8(nxt + e * SW + ctl_pos(c), base + (ss >> 1) * sw + c);
+      }
+    }
+#pragma unroll 1
+    for (int it = threadIdx.x; it < n; it += blockDim.x) {
+      const int jl = it / nthr;
+      const int q = it - jl * nthr;
+      const int4 J = sj[j0 + jl], X4 = sx[j0 + jl];
+      double* Z = base + J.z * sw;
+      double* W = X4.z >= 0 ? nxt + X4.z * SW : nullptr;
+      const double* X = cur + X4.x * SW;
+      if (J.w & 1) {  // copy job (executor.cpp:130-133): this thread's chains' coefficients
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          const int bq = h ? B - 1 - q : q;
+          if (h && bq == q) break;
+#pragma unroll
+          for (int r = 0; r < kCtlR; ++r) {
+            const int k = bq * kCtlR + r;
+            if (k <= d) {
+              const double v = X[ctl_pos(k)];
+              Z[k] = v;
+              if (W) W[ctl_pos(k)] = v;
+            }
+          }
+        }
+      } else if (!(a.dbg & 1)) {
+        ctl_pair_m1(X, cur + X4.y * SW, Z, W, q, B, d);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    if (a.stamps && threadIdx.x == 0) atomicMax(a.stamps + 1 + (sj[j0].w >> 8), global_ns());
+  }
+}
+
+// threads per block of k_conv_ctl: the lane kernels' count, except at M = 1
+// (real, no lanes) where a layer of p2 offers at most ~160 pair threads and
+// the register-blocked chains want more than the 64 registers a 1024-thread
+// block allows
+template <int M, bool CPLX>
+__host__ __device__ constexpr int ctl_threads() {
+  return M == 1 && !CPLX ? 256 : kConvThreads;
+}
+
+template <int M, bool CPLX>
+__global__ void __launch_bounds__(ctl_threads<M, CPLX>(), 1) k_conv_ctl(const CtlArgs a) {
+  extern __shared__ double smem[];
+  const Lane sm = make_lane(smem);
+  const int grp = blockIdx.x % a.ngroups;
+  double* base = a.arena + static_cast<int64_t>(blockIdx.x / a.ngroups) * a.G.point_words;
+  if (a.stamps) stamp_begin(a.stamps);
+  const int npairs = a.npairs;
+  if constexpr (M == 1 && !CPLX) {
+    ctl_group_m1(a, smem, grp, base);
+  } else {
+#pragma unroll 1
+    for (int L = a.group_off[grp]; L < a.group_off[grp + 1]; ++L) {
+      const int j0 = a.layer_off[L];
+      const int n = (a.layer_off[L + 1] - j0) * npairs;
+#pragma unroll 1
+      for (int it = threadIdx.x; it < n; it += blockDim.x)
+        conv_pair_at<M, CPLX, true>(a.jobs[j0 + it / npairs], base, a.G, it % npairs, sm);
+      __syncthreads();
+      if (a.stamps && threadIdx.x == 0) atomicMax(a.stamps + 1 + (a.jobs[j0].w >> 8), global_ns());
+    }
+  }
+}
+
 // ------------------------------------------------ split convolution (small)
 // Phase A: one thread per (point, job, product index). The product of a
 // complex coefficient pair is the (re, im) pair conv() adds to its
@@ -1239,6 +1535,21 @@ struct Impl {
     if (a.ngroups > 0) k_conv_cta<M, CPLX><<<static_cast<unsigned>(a.ngroups) * a.batch, kConvThreads, sh, s>>>(a);
     return true;
   }
+  // shared memory of k_conv_ctl: the lanes, or (M = 1, real) the staged series
+  // (M = 1: two stage buffers of max_stage series, then the largest group's
+  // tables, `table_bytes`)
+  static size_t smem_ctl(int max_stage, int d, size_t table_bytes) {
+    return M == 1 && !CPLX ? 2 * static_cast<size_t>(max_stage) * ctl_series_words() * sizeof(double) + table_bytes
+                           : smem_conv(kConvThreads);
+  }
+  static bool ctl_fits(int max_stage, int d, size_t table_bytes) {
+    return smem_ctl(max_stage, d, table_bytes) <= kCtaSmemMax && (!(M == 1 && !CPLX) || d + 1 <= kCtlR * kCtlLS);
+  }
+  static void conv_ctl(const CtlArgs& a, size_t table_bytes, cudaStream_t s) {
+    if (a.ngroups > 0)
+      k_conv_ctl<M, CPLX><<<static_cast<unsigned>(a.ngroups) * a.batch, ctl_threads<M, CPLX>(),
+                            smem_ctl(a.max_stage, a.G.d, table_bytes), s>>>(a);
+  }
   // resident blocks per SM: banded waves (flow = false) or the dataflow kernel
   static int band_blocks_per_sm(bool flow) {
     int nb = 0;
@@ -1292,6 +1603,7 @@ struct Impl {
     cudaFuncSetAttribute(k_conv<M, CPLX, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv_band<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, cc);
     cudaFuncSetAttribute(k_conv_cta<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCtaSmemMax));
+    cudaFuncSetAttribute(k_conv_ctl<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kCtaSmemMax));
     cudaFuncSetAttribute(k_conv_flow<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem_flow()));
     cudaFuncSetAttribute(k_conv_prod<M, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, c);
@@ -1302,7 +1614,7 @@ struct Impl {
     cudaFuncSetAttribute(k_md<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, o);
   }
   static const Launchers* table() {
-    static const Launchers L{&conv, &conv_band, &conv_flow, &band_blocks_per_sm, &conv_cta, &cta_fits, &conv_prod, &conv_accum, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE, kLaneThreads};
+    static const Launchers L{&conv, &conv_band, &conv_flow, &band_blocks_per_sm, &conv_cta, &cta_fits, &conv_ctl, &ctl_fits, &conv_prod, &conv_accum, &add, &scale, &extract, &md, &prepare, MdTraits<M>::LANE, kLaneThreads};
     return &L;
   }
 };

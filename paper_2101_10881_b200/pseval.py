@@ -475,7 +475,7 @@ class DevicePlan:
         check(lib().pse_plan_stream(self._h, C.byref(s)))
         return s.value or 0
 
-    CONV_PATHS = {1: "layered", 2: "waves", 3: "dataflow", 4: "hybrid", 5: "cta"}
+    CONV_PATHS = {1: "layered", 2: "waves", 3: "dataflow", 4: "hybrid", 5: "cta", 6: "cta_layers"}
 
     def conv_path(self, batch: int = 1) -> str:
         """the convolution path a run of `batch` points takes

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 LEVELS = [1, 2, 3, 4, 5, 8, 10]
 
 
-@pytest.fixture(params=["fused", "split", "band", "flow", "flow32", "cta"])
+@pytest.fixture(params=["fused", "split", "band", "flow", "flow32", "cta", "ctl"])
 def conv_path(request, monkeypatch):
     """Run an engine test through the fused conv kernel (one thread per
     coefficient pair), through the split path (products in parallel, then
@@ -27,11 +27,12 @@ def conv_path(request, monkeypatch):
     through its dataflow form (one persistent launch, per-task completion
     flags; 16- and 32-wide bands) and the CTA-local dataflow (one block per
     job group, shared-memory flags; where a group's flags do not fit next to
-    the lanes -- M >= 8 -- the global dataflow runs). The planner reads
+    the lanes -- M >= 8 -- the global dataflow runs) and the CTA-local layered
+    walk (one block per job group, its layers in order). The planner reads
     PSE_CONV_MODE and PSE_SPLIT_THRESHOLD when a plan is created: 0 forces
     fused, a huge value forces split."""
-    if request.param == "cta":
-        monkeypatch.setenv("PSE_CONV_MODE", "cta")
+    if request.param in ("cta", "ctl"):
+        monkeypatch.setenv("PSE_CONV_MODE", request.param)
     elif request.param in ("band", "flow", "flow32"):
         # waves use 32-wide bands, the dataflow kernel 16 (flow32: 32)
         monkeypatch.setenv("PSE_CONV_MODE", request.param[:4])

@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "ctl" -x > gpurun_out/r2b_pytest_ctl.log 2>&1; echo "pytest rc=$?"; grep -E "FAILED|passed|failed" gpurun_out/r2b_pytest_ctl.log | tail -5
+python tools/diag/layers.py --workload c3 --m 1
+PSE_CTL_DBG=2 python tools/diag/layers.py --workload c3 --m 1
