@@ -27,6 +27,8 @@
  *   pse_md_apply                          <- md_add / md_sub / md_mul (multidouble.hpp:75-94 ->
  *                                            expansion.hpp:142-211), elementwise on arrays
  *   pse_series_conv                       <- Series conv(const Series&, const Series&)  src/pseries.cpp:37-64
+ *   pse_series_add                        <- Series series_add(const Series&, const Series&)  src/pseries.cpp:66-74
+ *   pse_series_scale_int                  <- Series series_scale_int(const Series&, long)  src/pseries.cpp:85-93
  *   pse_eval_direct                       <- Evaluation eval_direct(const Polynomial&, const std::vector<Series>&)
  *                                            include/pseval/oracle.hpp, src/oracle_direct.cpp:41-78
  *   pse_plan_layer_ms                     <- RunReport::conv_layer_ms / add_layer_ms  executor.hpp:31-43
@@ -270,6 +272,14 @@ int pse_md_apply(int32_t op, int32_t m, int32_t impl, int64_t count, const doubl
 /* z = conv(x, y) for `count` independent pairs; x, y, z: [count][Q][d+1] */
 int pse_series_conv(int32_t d, int32_t m, int32_t mode, int64_t count, const double* x, const double* y,
                     double* z, int32_t device);
+/* z = series_add(x, y) (pseries.cpp:66-74: md_add per coefficient, x first)
+ * and z = series_scale_int(x, factor) (pseries.cpp:85-93: md_mul by
+ * md_from_double(factor); |factor| < 2^31) for `count` independent items;
+ * x, y, z: [count][Q][d+1] */
+int pse_series_add(int32_t d, int32_t m, int32_t mode, int64_t count, const double* x, const double* y,
+                   double* z, int32_t device);
+int pse_series_scale_int(int32_t d, int32_t m, int32_t mode, int64_t count, const double* x, int64_t factor,
+                         double* z, int32_t device);
 
 /* pinned host memory for end-to-end transfers */
 void* pse_host_alloc(size_t bytes);

@@ -6,5 +6,5 @@ from .pseval import *  # noqa: F401,F403
 from .pseval import (CPLX, REAL, DataArray, DevicePlan, JobGraph, Monomial, OpCost, Polynomial, Problem,
                      RunReport, build_jobgraph, build_jobgraph_shape, evaluate, evaluate_packed, flop_count,
                      flop_count_add, flop_count_mul, gen_benchmark, instrumented_cost, md_apply, reporting_cost,
-                     run_device, series_conv, stage, validate)
+                     run_device, series_add, series_conv, series_scale_int, stage, validate)
 from ._lib import InvalidArgument, PseError, LIB_PATH

@@ -60,7 +60,8 @@ EXPORTS = [
     "pse_graph_validate", "pse_flop_count", "pse_cost", "pse_gen_benchmark_size", "pse_gen_benchmark",
     "pse_plan_create", "pse_plan_destroy", "pse_plan_upload", "pse_plan_execute", "pse_plan_download",
     "pse_plan_run", "pse_plan_info", "pse_plan_stream", "pse_plan_conv_path", "pse_band_schedule_stats", "pse_plan_arena_ipc_handle",
-    "pse_plan_open_peer", "pse_plan_set_peer_arena", "pse_plan_gather_peers", "pse_evaluate", "pse_md_apply", "pse_series_conv", "pse_host_alloc",
+    "pse_plan_open_peer", "pse_plan_set_peer_arena", "pse_plan_gather_peers", "pse_evaluate", "pse_md_apply", "pse_series_conv", "pse_series_add",
+    "pse_series_scale_int", "pse_host_alloc",
     "pse_host_free", "pse_device_info", "pse_fp64_peak",
     "pse_problem_parse", "pse_problem_read", "pse_problem_write", "pse_problem_text", "pse_problem_create",
     "pse_problem_gen", "pse_problem_info", "pse_problem_id", "pse_problem_arrays", "pse_problem_destroy",
@@ -111,6 +112,8 @@ def lib():
     L.pse_evaluate.argtypes = [i32, i32, i32, i32, i32, dp, dp, dp, i32, dp, dp, i32, C.POINTER(Report)]
     L.pse_md_apply.argtypes = [i32, i32, i32, i64, dp, dp, dp, i32]
     L.pse_series_conv.argtypes = [i32, i32, i32, i64, dp, dp, dp, i32]
+    L.pse_series_add.argtypes = [i32, i32, i32, i64, dp, dp, dp, i32]
+    L.pse_series_scale_int.argtypes = [i32, i32, i32, i64, dp, i64, dp, i32]
     L.pse_host_alloc.argtypes = [C.c_size_t]
     L.pse_host_alloc.restype = C.c_void_p
     L.pse_host_free.argtypes = [_VP]

@@ -1916,6 +1916,81 @@ int pse_series_conv(int32_t d, int32_t m, int32_t mode, int64_t count, const dou
   });
 }
 
+extern "C++" {
+namespace pse {
+// one-shot device run of a series primitive over `count` independent items of
+// `nslots` series each (host layout [count][nslots][Q][d+1]); `launch` gets
+// the arena and geometry, slot 0 comes back as the result
+template <class F>
+int series_oneshot(int32_t d, int32_t m, int32_t mode, int64_t count, int nslots, const double* const* in,
+                   double* z, int32_t device, F&& launch) {
+  if (!valid_precision(m) || d < 0 || count < 0 || count > (int64_t(1) << 31) / (d + 1))
+    throw std::invalid_argument("bad series arguments");
+  if (count == 0) return PSE_OK;
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  Geom G;
+  G.d = d;
+  G.S = d + 1;
+  G.Q = (mode == PSE_MODE_COMPLEX ? 2 : 1) * m;
+  G.slot_words = static_cast<int64_t>(G.Q) * G.S;
+  G.point_words = nslots * G.slot_words;
+  const int64_t sw = G.slot_words;
+  double* arena;
+  ck(cudaMalloc(&arena, static_cast<size_t>(count) * G.point_words * sizeof(double)), "cudaMalloc");
+  for (int sl = 0; sl < nslots; ++sl)
+    ck(cudaMemcpy2D(arena + sl * sw, nslots * sw * sizeof(double), in[sl], sw * sizeof(double), sw * sizeof(double),
+                    count, cudaMemcpyHostToDevice),
+       "H2D");
+  const Launchers* L = launchers_for(m, mode == PSE_MODE_COMPLEX);
+  L->prepare();
+  launch(L, arena, G);
+  ck(cudaGetLastError(), "series launch");
+  ck(cudaMemcpy2D(z, sw * sizeof(double), arena, nslots * sw * sizeof(double), sw * sizeof(double), count,
+                  cudaMemcpyDeviceToHost),
+     "D2H");
+  cudaFree(arena);
+  return PSE_OK;
+}
+}  // namespace pse
+}  // extern "C++"
+
+int pse_series_add(int32_t d, int32_t m, int32_t mode, int64_t count, const double* x, const double* y, double* z,
+                   int32_t device) {
+  return pse::guarded([&] {
+    const double* in[2] = {x, y};
+    return pse::series_oneshot(d, m, mode, count, 2, in, z, device, [&](const pse::Launchers* L, double* arena,
+                                                                        const pse::Geom& G) {
+      int2* job;
+      pse::ck(cudaMalloc(&job, sizeof(int2)), "cudaMalloc");
+      const int2 hj = make_int2(1, 0);  // slot 0 := md_add(slot 0, slot 1)
+      pse::ck(cudaMemcpy(job, &hj, sizeof hj, cudaMemcpyHostToDevice), "H2D");
+      pse::AddArgs a{arena, G, job, 1, static_cast<int>(count), nullptr, nullptr};
+      L->add(a, nullptr);
+      pse::ck(cudaDeviceSynchronize(), "series add");
+      cudaFree(job);
+    });
+  });
+}
+
+int pse_series_scale_int(int32_t d, int32_t m, int32_t mode, int64_t count, const double* x, int64_t factor,
+                         double* z, int32_t device) {
+  return pse::guarded([&] {
+    if (factor > INT32_MAX || factor < INT32_MIN) throw std::invalid_argument("factor out of range");
+    const double* in[1] = {x};
+    return pse::series_oneshot(d, m, mode, count, 1, in, z, device, [&](const pse::Launchers* L, double* arena,
+                                                                        const pse::Geom& G) {
+      int2* item;
+      pse::ck(cudaMalloc(&item, sizeof(int2)), "cudaMalloc");
+      const int2 hi = make_int2(0, static_cast<int>(factor));
+      pse::ck(cudaMemcpy(item, &hi, sizeof hi, cudaMemcpyHostToDevice), "H2D");
+      pse::ScaleArgs a{arena, G, item, 1, static_cast<int>(count), nullptr, nullptr};
+      L->scale(a, nullptr);
+      pse::ck(cudaDeviceSynchronize(), "series scale");
+      cudaFree(item);
+    });
+  });
+}
+
 void* pse_host_alloc(size_t bytes) {
   void* p = nullptr;
   if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {

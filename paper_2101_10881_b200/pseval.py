@@ -747,6 +747,25 @@ def series_conv(x: np.ndarray, y: np.ndarray, mode: str = REAL, device: int = 0)
     return z
 
 
+def series_add(x: np.ndarray, y: np.ndarray, mode: str = REAL, device: int = 0) -> np.ndarray:
+    """series_add (pseries.cpp:66-74) of count pairs: x, y [count][P][m][d+1]."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    count, P, m, d1 = x.shape
+    z = np.empty_like(x)
+    check(lib().pse_series_add(d1 - 1, m, _mode_code(mode), count, ptr(x), ptr(y), ptr(z), device))
+    return z
+
+
+def series_scale_int(x: np.ndarray, factor: int, mode: str = REAL, device: int = 0) -> np.ndarray:
+    """series_scale_int (pseries.cpp:85-93) of count series: x [count][P][m][d+1]."""
+    x = np.ascontiguousarray(x, np.float64)
+    count, P, m, d1 = x.shape
+    z = np.empty_like(x)
+    check(lib().pse_series_scale_int(d1 - 1, m, _mode_code(mode), count, ptr(x), int(factor), ptr(z), device))
+    return z
+
+
 def device_info(device: int = 0):
     out = np.zeros(4, np.int64)
     check(lib().pse_device_info(device, ptr(out)))

@@ -120,6 +120,26 @@ def test_series_conv_bitwise(m, cplx):
             assert_bitwise(z[c], po.series_conv(x[c], y[c], cplx), f"conv d={d} m={m} c={c}")
 
 
+@pytest.mark.parametrize("m", LEVELS)
+@pytest.mark.parametrize("cplx", [False, True])
+def test_series_add_and_scale_bitwise(m, cplx):
+    """series_add / series_scale_int (pseries.cpp:66-93) over the C ABI equal
+    the oracle's md_add / md_mul by md_from_double(c) per coefficient."""
+    rng = np.random.default_rng(20 * m + cplx)
+    P, d, cnt = (2 if cplx else 1), 17, 4
+    x = po.random_md(int(rng.integers(1, 2**60)), m, cnt * P * (d + 1)).reshape(cnt, P, d + 1, m).transpose(0, 1, 3, 2).copy()
+    y = po.random_md(int(rng.integers(1, 2**60)), m, cnt * P * (d + 1)).reshape(cnt, P, d + 1, m).transpose(0, 1, 3, 2).copy()
+    mode = "cplx" if cplx else "real"
+    flat = lambda a: a.transpose(0, 1, 3, 2).reshape(-1, m).copy()  # [count*P*(d+1)][m]
+    z = pe.series_add(x, y, mode)
+    assert_bitwise(flat(z), po.md_op("add", flat(x), flat(y)), f"series_add m={m}")
+    for c in (3, -7, 0, 1 << 20):
+        cm = np.zeros_like(flat(x))
+        cm[:, 0] = float(c)
+        z = pe.series_scale_int(x, c, mode)
+        assert_bitwise(flat(z), po.md_op("mul", flat(x), cm), f"series_scale_int c={c} m={m}")
+
+
 # ---------------------------------------------------------------- whole engine
 def test_c1_bitwise_vs_reference_engine(conv_path):
     """C1: p1, d=15, m=2, seed 7 -- value, all 16 gradients and the whole

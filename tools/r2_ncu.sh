@@ -6,7 +6,7 @@
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_bench_c2.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu > /dev/null 2>&1; echo "launches rc=$?"
-ncu --set full --import-source on --clock-control none -k regex:'k_conv<' -s 1 -c 1 -o gpurun_out/r2_conv_c2 -f \
+ncu --set full --import-source on --clock-control none -k k_conv -s 1 -c 1 -o gpurun_out/r2_conv_c2 -f \
   python tools/profile_run.py --workload c2 > /dev/null 2>&1; echo "conv rc=$?"
 ncu --set full --import-source on --clock-control none -k regex:k_conv_flow -c 1 -o gpurun_out/r2_flow_c3h -f \
   python tools/profile_run.py --workload c3h > /dev/null 2>&1; echo "flow rc=$?"
