@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -k "ctl or series_add" -x > gpurun_out/r2b_pytest_ctl.log 2>&1; echo "pytest rc=$?"; grep -E "FAILED|passed|failed" gpurun_out/r2b_pytest_ctl.log | tail -5
+python tools/diag/layers.py --workload c3 --m 1
+PSE_LIB_VARIANT=ctlpair python tools/diag/layers.py --workload c3 --m 1
+python tools/variant_time.py --workload c3 --m 1
+PSE_LIB_VARIANT=ctlpair python tools/variant_time.py --workload c3 --m 1
