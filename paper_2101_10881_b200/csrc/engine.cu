@@ -600,13 +600,6 @@ struct Plan {
     return conv_mode == 4 || conv_mode == 5 ||
            (conv_mode == 0 && m == 1 && ncomps > 0 && ncomps <= 2 * sms && nrows_mine >= int64_t(32) * ncomps);
   }
-  static int ctl_dbg() {
-    static const int v = [] {
-      const char* e = getenv("PSE_CTL_DBG");
-      return e ? atoi(e) : 0;
-    }();
-    return v;
-  }
   bool cta_layered() const { return conv_mode == 5 || (conv_mode == 0 && m == 1); }
   bool cta_mode() const { return prefer_cta() && cta_ready(); }
   bool cta_ready() const { return cta.built && cta.ok; }
@@ -933,7 +926,7 @@ struct Plan {
     }
     if (first < static_cast<int>(layer_rows.size()) && cta_mode() && cta.layered) {  // CTA-local layers
       CtlArgs a{arena,         G,          cta.ljobs, cta.layer_off,  cta.lgroup_off, cta.ngroups, batch, (d + 2) / 2,
-                stamps,        cta.stage_off, cta.stage_slot, cta.sidx, cta.gjob_off, cta.max_stage, ctl_dbg()};
+                stamps,        cta.stage_off, cta.stage_slot, cta.sidx, cta.gjob_off, cta.max_stage};
       L->conv_ctl(a, cta.table_bytes, stream);
       ++launches;
     } else if (first < static_cast<int>(layer_rows.size()) && cta_mode()) {  // CTA-local dataflow

@@ -221,7 +221,6 @@ struct CtlArgs {
   const int4* sidx;       // per job: staged (in1, in2) in its layer's list, its out in the next layer's (or -1)
   const int* gjob_off;    // [ngroups+1] first job of each group
   int max_stage;          // longest list
-  int dbg;                // timing experiments only (PSE_CTL_DBG): 1 skips the chains, 2 the prefetch
 };
 
 struct Launchers {
@@ -1139,7 +1138,7 @@ __device__ __forceinline__ void ctl_group_m1(const CtlArgs& a, double* smem_d, i
     const double* cur = (l & 1) ? buf1 : buf0;
     double* nxt = (l & 1) ? buf0 : buf1;
     const int j0 = loff[l], n = (loff[l + 1] - j0) * nthr;
-    if (l + 1 < nl && !(a.dbg & 2)) {
+    if (l + 1 < nl) {
       // prefetch the next layer's inputs that this layer does not produce,
       // by the threads without chains first (counted from the last thread)
       const int e0 = soff[l + 1], nw = (soff[l + 2] - e0) * n1;
@@ -1172,7 +1171,7 @@ __device__ __forceinline__ void ctl_group_m1(const CtlArgs& a, double* smem_d, i
             }
           }
         }
-      } else if (!(a.dbg & 1)) {
+      } else {
         ctl_pair_m1(X, cur + X4.y * SW, Z, W, q, B, d);
       }
     }
