@@ -985,116 +985,85 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // M = 1 chains in register blocks. A job's d+1 chains z_k = sum_i x_i y_{k-i}
-// (ascending i, pseries.cpp:41-48) are cut into blocks of kCtlR = 2 adjacent
-// chains k0, k0+1 (k0 = 2b, B = ceil((d+1)/2) blocks); thread q of a job
-// runs block nB = B-1-q and, when distinct, block nA = q side by side, one
-// step of each per step s: the chains of both blocks need x_s, chain r of a
-// block needs y_{k0+r-s} -- the element chain r-1 used one step earlier --
-// so a step is one x load, two y loads and four independent DMUL + DADD
-// pairs. The loop runs block B's chunks (2 steps each); block A's chains end
-// inside it (chain r after step 2nA + r), where their sums are copied out
-// (predicated), and then run on over padding words that nothing stores. An
-// accumulator starts at -0 (x + -0 == x bitwise for every x, so the first
-// sum is the first product, as in the reference).
-//
-// Staged series are stored transposed by two -- element j at (j % 2) *
-// kCtlLS + kCtlOff + j / 2 -- so that the y loads of the lanes of a warp
-// (consecutive q of one job) hit consecutive words (x_s is a broadcast), with
-// kCtlOff words of padding in front of each half for block A's overrun.
-constexpr int kCtlR = 2;
-constexpr int kCtlLS = 256;  // half-series stride: d + 1 <= 256
-constexpr int kCtlOff = 128;
+// (ascending i, pseries.cpp:41-48) are cut into blocks of kCtlR adjacent
+// chains; thread b of a job runs block b (ctl_block_m1). kCtlR = 3 and four
+// chunks per loop trip measured best on C3 at m=1 (conv stage 0.164 ms; R = 2:
+// 0.174, 4: 0.202, 5: 0.202; one chain per thread 0.220; pairs of blocks
+// b and B-1-b per thread, side by side or one after the other, 0.242-0.248;
+// pairs of single chains (k, d-k) 0.252). An accumulator starts at -0
+// (x + -0 == x bitwise for every x, so the first sum is the first product,
+// as in the reference).
+#ifndef PSE_CTL_R
+#define PSE_CTL_R 3
+#endif
+#ifndef PSE_CTL_UNROLL
+#define PSE_CTL_UNROLL 4
+#endif
+constexpr int kCtlR = PSE_CTL_R;
+constexpr int kCtlUnroll = PSE_CTL_UNROLL;
+constexpr int kCtlOff = 8;           // words in front of each sub-series (the loop's look-ahead)
+constexpr int kCtlLS = 512 / kCtlR;  // sub-series stride: d + 1 <= kCtlR * (kCtlLS - kCtlOff - 1)
 __host__ __device__ constexpr int ctl_series_words() { return kCtlR * kCtlLS; }
-__device__ __forceinline__ int ctl_pos(int j) { return (j & 1) * kCtlLS + kCtlOff + (j >> 1); }
+__device__ __forceinline__ int ctl_pos(int j) { return (j % kCtlR) * kCtlLS + kCtlOff + j / kCtlR; }
 
-// thread q's chains of one job (X, Y staged; Z the arena series; W the next
-// layer's staged copy of Z or null). The operands of chunk u+1 are loaded
-// before chunk u computes (a warp issues in order: a load placed after the
-// chunk's sums would put the load -> DMUL -> DADD latency on every chunk);
-// chunks go in pairs so the two operand sets swap roles without copies.
-__device__ __forceinline__ void ctl_pair_m1(const double* X, const double* Y, double* Z, double* W, int q, int B, int d) {
-  constexpr int LS = kCtlLS;
-  const int nA = q, nB = B - 1 - q;
-  const bool hasA = nA < nB;
+// One register block of R adjacent M = 1 chains (k0 = bR .. k0+R-1) per
+// thread: steps s = 0..k0+R-1 taken R at a time (a "chunk"), the block's
+// chains sharing x_s and chain r reusing the y element chain r-1 used one
+// step earlier (a ring of R registers), so a step is one x load (a
+// broadcast), one y load and R independent DMUL + DADD pairs. The last chunk
+// is peeled (chain k0+r ends at its step r). Operands one chunk ahead.
+// Staged series are transposed by R (element j at (j % R) * kCtlLS +
+// kCtlOff + j / R): the y loads of a warp (consecutive b) are consecutive
+// words.
+__device__ __forceinline__ void ctl_block_m1(const double* X, const double* Y, double* Z, double* W, int b, int d) {
+  constexpr int R = kCtlR, LS = kCtlLS;
   const double* px = X + kCtlOff;
-  const double* pa = Y + kCtlOff + nA;  // y_{2(b-u)} at pa[0], y_{2(b-u)-1} at pa[LS-1]
-  const double* pb = Y + kCtlOff + nB;
-  double a0 = -0.0, a1 = -0.0, b0 = -0.0, b1 = -0.0;  // chains k0, k0+1 of blocks A, B
-  double sa0 = 0.0, sa1 = 0.0;                       // block A's results
-  double wa1 = pa[LS], wb1 = pb[LS];                 // y_{k0+1}
-  struct Ops {
-    double x0, x1, ya0, ya1, yb0, yb1;  // x_s, x_{s+1}; y_{k0-s}, y_{k0-s-1} of A and B
+  const double* py = Y + kCtlOff + b;  // y_{R(b-u)} at py[0], y_{R(b-u)-j} at py[(R-j) LS - 1]
+  double acc[R], w[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = -0.0;
+#pragma unroll
+  for (int r = 1; r < R; ++r) w[r] = py[r * LS];  // y_{k0+r}
+  double xc[R], yc[R];
+  auto load = [&](double (&xv)[R], double (&yv)[R]) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      xv[j] = px[j * LS];
+      yv[j] = j == 0 ? py[0] : py[(R - j) * LS - 1];
+    }
   };
-  auto load = [&](Ops& o) {
-    o.x0 = px[0];
-    o.x1 = px[LS];
-    o.ya0 = pa[0];
-    o.ya1 = pa[LS - 1];
-    o.yb0 = pb[0];
-    o.yb1 = pb[LS - 1];
-  };
-  // one chunk: steps s = 2u, 2u+1. Ring: at step s chain r uses y_{k0+r-s}.
-  auto chunk = [&](const Ops& o, int u) {
-    // s = 2u: chain 0 <- y_{k0-s} (new), chain 1 <- y_{k0+1-s} (w1)
-    a0 = __dadd_rn(a0, __dmul_rn(o.x0, o.ya0));
-    a1 = __dadd_rn(a1, __dmul_rn(o.x0, wa1));
-    b0 = __dadd_rn(b0, __dmul_rn(o.x0, o.yb0));
-    b1 = __dadd_rn(b1, __dmul_rn(o.x0, wb1));
-    const bool endA = u == nA;
-    sa0 = endA ? a0 : sa0;  // chain 2nA of block A ends at this step
-    // s = 2u+1: chain 0 <- y_{k0-s} (new), chain 1 <- y_{k0+1-s} = y_{k0-2u}
-    a1 = __dadd_rn(a1, __dmul_rn(o.x1, o.ya0));
-    a0 = __dadd_rn(a0, __dmul_rn(o.x1, o.ya1));
-    b1 = __dadd_rn(b1, __dmul_rn(o.x1, o.yb0));
-    b0 = __dadd_rn(b0, __dmul_rn(o.x1, o.yb1));
-    sa1 = endA ? a1 : sa1;
-    wa1 = o.ya1;  // y_{k0+1-(s+2)}
-    wb1 = o.yb1;
-  };
-  auto advance = [&]() {
+  load(xc, yc);
+#pragma unroll kCtlUnroll
+  for (int u = 0; u < b; ++u) {
     ++px;
-    --pa;
-    --pb;
-  };
-  Ops o0, o1;
-  load(o0);
-  int u = 0;
-#pragma unroll 1
-  for (; u + 2 <= nB; u += 2) {
-    advance();
-    load(o1);
-    chunk(o0, u);
-    advance();
-    load(o0);
-    chunk(o1, u + 1);
+    --py;
+    double xn[R], yn[R];
+    load(xn, yn);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      w[(R - j) % R] = yc[j];  // y_{k0-s}, s = uR + j
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = __dadd_rn(acc[r], __dmul_rn(xc[j], w[(r - j + R) % R]));
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      xc[j] = xn[j];
+      yc[j] = yn[j];
+    }
   }
-  if (u < nB) {
-    advance();
-    load(o1);
-    chunk(o0, u);
-    o0 = o1;
-    ++u;
+  // last chunk (u = b): chain r ends at step j = r
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    w[(R - j) % R] = yc[j];
+#pragma unroll
+    for (int r = j; r < R; ++r) acc[r] = __dadd_rn(acc[r], __dmul_rn(xc[j], w[(r - j + R) % R]));
   }
-  // block B's last chunk (u == nB): chain 2nB ends at its first step
-  b0 = __dadd_rn(b0, __dmul_rn(o0.x0, o0.yb0));
-  b1 = __dadd_rn(b1, __dmul_rn(o0.x0, wb1));
-  b1 = __dadd_rn(b1, __dmul_rn(o0.x1, o0.yb0));
-  const int kb = 2 * nB;
-  if (kb <= d) {
-    Z[kb] = b0;
-    if (W) W[ctl_pos(kb)] = b0;
-  }
-  if (kb + 1 <= d) {
-    Z[kb + 1] = b1;
-    if (W) W[ctl_pos(kb + 1)] = b1;
-  }
-  if (hasA) {
-    const int ka = 2 * nA;
-    Z[ka] = sa0;
-    Z[ka + 1] = sa1;
-    if (W) {
-      W[ctl_pos(ka)] = sa0;
-      W[ctl_pos(ka + 1)] = sa1;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int k = b * R + r;
+    if (k <= d) {
+      Z[k] = acc[r];
+      if (W) W[r * LS + kCtlOff + b] = acc[r];
     }
   }
 }
@@ -1103,7 +1072,7 @@ __device__ __forceinline__ void ctl_pair_m1(const double* X, const double* Y, do
 __device__ __forceinline__ void ctl_group_m1(const CtlArgs& a, double* smem_d, int grp, double* base) {
   const int d = a.G.d, n1 = d + 1;
   constexpr int SW = ctl_series_words();
-  const int B = (d + kCtlR) / kCtlR, nthr = (B + 1) / 2;  // blocks and threads per job
+  const int nthr = (d + kCtlR) / kCtlR;  // register blocks = threads per job
   const int64_t sw = a.G.slot_words;
   const int jb0 = a.gjob_off[grp], nj = a.gjob_off[grp + 1] - jb0;
   const int lb0 = a.group_off[grp], nl = a.group_off[grp + 1] - lb0;
@@ -1156,23 +1125,14 @@ __device__ __forceinline__ void ctl_group_m1(const CtlArgs& a, double* smem_d, i
       double* Z = base + J.z * sw;
       double* W = X4.z >= 0 ? nxt + X4.z * SW : nullptr;
       const double* X = cur + X4.x * SW;
-      if (J.w & 1) {  // copy job (executor.cpp:130-133): this thread's chains' coefficients
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          const int bq = h ? B - 1 - q : q;
-          if (h && bq == q) break;
-#pragma unroll
-          for (int r = 0; r < kCtlR; ++r) {
-            const int k = bq * kCtlR + r;
-            if (k <= d) {
-              const double v = X[ctl_pos(k)];
-              Z[k] = v;
-              if (W) W[ctl_pos(k)] = v;
-            }
-          }
+      if (J.w & 1) {  // copy job (executor.cpp:130-133): this thread's block of coefficients
+        for (int k = kCtlR * q; k < kCtlR * (q + 1) && k <= d; ++k) {
+          const double v = X[ctl_pos(k)];
+          Z[k] = v;
+          if (W) W[ctl_pos(k)] = v;
         }
       } else {
-        ctl_pair_m1(X, cur + X4.y * SW, Z, W, q, B, d);
+        ctl_block_m1(X, cur + X4.y * SW, Z, W, q, d);
       }
     }
     cp_async_wait_all();
@@ -1182,12 +1142,11 @@ __device__ __forceinline__ void ctl_group_m1(const CtlArgs& a, double* smem_d, i
 }
 
 // threads per block of k_conv_ctl: the lane kernels' count, except at M = 1
-// (real, no lanes) where a layer of p2 offers at most ~160 pair threads and
-// the register-blocked chains want more than the 64 registers a 1024-thread
-// block allows
+// (real, no lanes): a layer of p2 has at most 4 jobs x 51 register blocks,
+// and the blocks want more than the 64 registers a 1024-thread block allows
 template <int M, bool CPLX>
 __host__ __device__ constexpr int ctl_threads() {
-  return M == 1 && !CPLX ? 256 : kConvThreads;
+  return M == 1 && !CPLX ? 320 : kConvThreads;
 }
 
 template <int M, bool CPLX>
@@ -1542,7 +1501,8 @@ struct Impl {
                            : smem_conv(kConvThreads);
   }
   static bool ctl_fits(int max_stage, int d, size_t table_bytes) {
-    return smem_ctl(max_stage, d, table_bytes) <= kCtaSmemMax && (!(M == 1 && !CPLX) || d + 1 <= kCtlR * kCtlLS);
+    return smem_ctl(max_stage, d, table_bytes) <= kCtaSmemMax &&
+           (!(M == 1 && !CPLX) || d + 1 <= kCtlR * (kCtlLS - kCtlOff - 1));
   }
   static void conv_ctl(const CtlArgs& a, size_t table_bytes, cudaStream_t s) {
     if (a.ngroups > 0)
