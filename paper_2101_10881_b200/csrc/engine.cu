@@ -585,20 +585,16 @@ struct Plan {
     size_t table_bytes = 0;
   } cta;
 
-  // The CTA-local path is taken when forced (PSE_CONV_MODE=cta) and, by
-  // default, at M = 1 for deep graphs of few large job groups (a block per
-  // group still fills the GPU, and the group's chains are long): there a
-  // task's arithmetic is a DMUL + DADD per step and the global dataflow
-  // kernel's per-task L2 round trips dominate (C3 / C3' m=1: 0.92 / 1.16 ->
-  // 0.39 ms). Many small groups (p1, p3) stay on the global kernel (C2 m=1:
-  // 0.22 vs 0.61 ms CTA-local); at M >= 2 the global kernel is faster.
-  //
-  // At M = 1 the default is the layered form (k_conv_ctl): a step is one
-  // DMUL + DADD, so even a layer-by-layer walk of p2's 64 layers is short
-  // next to the band tasks' hand-out and flag costs (C3 m=1: see DESIGN).
+  // The CTA-local paths are taken when forced (PSE_CONV_MODE=cta: the band
+  // tasks' dataflow, PSE_CONV_MODE=ctl: the layer walk) and, by default, for
+  // every real graph at M = 1: the layer walk (k_conv_ctl) with the group's
+  // operands in shared memory, whatever the group sizes -- C3 m=1 0.165 ms
+  // conv (CTA-local dataflow 0.355, global dataflow 0.92), C2 m=1 0.091
+  // (hybrid 0.30), C4 m=1 0.246 (layered 0.40), C1 m=1 0.031 (dataflow
+  // 0.038). At M >= 2 the global kernels are faster (C3 m=2: dataflow 4.3 ms,
+  // CTA-local dataflow 5.1, layer walk 8-17).
   bool prefer_cta() const {
-    return conv_mode == 4 || conv_mode == 5 ||
-           (conv_mode == 0 && m == 1 && ncomps > 0 && ncomps <= 2 * sms && nrows_mine >= int64_t(32) * ncomps);
+    return conv_mode == 4 || conv_mode == 5 || (conv_mode == 0 && m == 1 && P == 1 && ncomps > 0);
   }
   bool cta_layered() const { return conv_mode == 5 || (conv_mode == 0 && m == 1); }
   bool cta_mode() const { return prefer_cta() && cta_ready(); }

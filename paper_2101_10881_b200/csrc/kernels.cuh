@@ -1076,6 +1076,7 @@ __device__ __forceinline__ void ctl_group_m1(const CtlArgs& a, double* smem_d, i
   const int64_t sw = a.G.slot_words;
   const int jb0 = a.gjob_off[grp], nj = a.gjob_off[grp + 1] - jb0;
   const int lb0 = a.group_off[grp], nl = a.group_off[grp + 1] - lb0;
+  if (nl == 0) return;  // a group without conv jobs on this rank (sharded plans)
   const int sb0 = a.stage_off[lb0], ns = a.stage_off[lb0 + nl] - sb0;
   // shared memory: the two stage buffers, then the group's tables
   double* buf0 = smem_d;

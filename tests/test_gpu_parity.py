@@ -392,7 +392,8 @@ def test_reference_binding_drop_in():
     assert "OK: RunReport per-layer timings" in r.stdout, r.stdout
 
 
-@pytest.mark.parametrize("pid,d,m,nranks", [("p1", 15, 2, 2), ("p1", 8, 4, 3), ("p3", 4, 2, 4), ("p2", 3, 3, 2)])
+@pytest.mark.parametrize("pid,d,m,nranks", [("p1", 15, 2, 2), ("p1", 8, 4, 3), ("p3", 4, 2, 4), ("p2", 3, 3, 2),
+                                             ("p1", 15, 1, 3), ("p3", 4, 1, 4)])
 def test_monomial_sharding_is_bit_exact(pid, d, m, nranks):
     """One polynomial sharded over nranks plans (here all on device 0): each
     runs its monomials' conv jobs, the term blocks are exchanged, each runs the
@@ -426,7 +427,7 @@ def test_monomial_sharding_is_bit_exact(pid, d, m, nranks):
     assert_bitwise(ref_vg[:, 0].reshape(want.shape), want, "vs oracle")
 
 
-@pytest.mark.parametrize("pid,d,m,nranks", [("p1", 15, 2, 2), ("p3", 4, 2, 4), ("p2", 40, 3, 3)])
+@pytest.mark.parametrize("pid,d,m,nranks", [("p1", 15, 2, 2), ("p3", 4, 2, 4), ("p2", 40, 3, 3), ("p2", 40, 1, 3)])
 def test_monomial_sharding_peer_gather_is_bit_exact(pid, d, m, nranks):
     """The same sharding with the exchange done by pse_plan_gather_peers: each
     rank copies the slots the other ranks produced straight out of their
@@ -697,17 +698,19 @@ def test_sharded_report_times_the_exchange_on_the_device():
         assert abs(fin.conv_ms + fin.exchange_ms + fin.scale_ms + fin.add_ms - fin.wall_ms) <= 1e-6 * fin.wall_ms + 1e-6
 
 
-def test_sharded_plan_with_an_empty_rank():
+@pytest.mark.parametrize("m", [1, 2])
+def test_sharded_plan_with_an_empty_rank(m):
     """more ranks than independent job groups (one monomial, 3 ranks): the
     ranks without conv jobs still run the exchange and the exact addition
-    tree, and every rank's result equals one device's"""
+    tree, and every rank's result equals one device's (m=1: the CTA-local
+    layer walk with groups that have no jobs on a rank)"""
     pe_g = pe.GraphArrays  # noqa: F841 (import check)
     rng = np.random.default_rng(11)
-    p = md_instance(rng, 2, False, nmax=3, Nmax=1, dmin=5, dmax=5)
+    p = md_instance(rng, m, False, nmax=3, Nmax=1, dmin=5, dmax=5)
     g = pe.build_jobgraph_shape(p.n, p.d, p.nvars, p.idx)
     st = p.stat.reshape(p.P * p.m, *p.stat.shape[2:])
-    want, _, _ = pe.DevicePlan(g, 2, "real", 0, 1).run(st, 1)
-    plans = [pe.DevicePlan(g, 2, "real", 0, 1, rank=r, nranks=3) for r in range(3)]
+    want, _, _ = pe.DevicePlan(g, m, "real", 0, 1).run(st, 1)
+    plans = [pe.DevicePlan(g, m, "real", 0, 1, rank=r, nranks=3) for r in range(3)]
     for p1 in plans:
         for p2 in plans:
             if p2 is not p1:
