@@ -226,17 +226,18 @@ def test_multiband_md_instances(m, cplx, conv_path):
         assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"md instance m={m} cplx={cplx} d={p.d} it={it}")
 
 
-def test_batched_points_equal_single_points(conv_path):
+@pytest.mark.parametrize("m", [4, 1])
+def test_batched_points_equal_single_points(conv_path, m):
     """one launch per layer across a batch of points == each point alone."""
     rng = np.random.default_rng(42)
-    base = po.gen_benchmark("p1", 12, 4, seed=7)
+    base = po.gen_benchmark("p1", 12, m, seed=7)
     B = 5
     Q = base.P * base.m
     top = base.stat.shape[2]
     stat = np.empty((Q, B, top, 13))
     refs = []
     for b in range(B):
-        zb = po.gen_benchmark("p1", 12, 4, seed=1000 + b)
+        zb = po.gen_benchmark("p1", 12, m, seed=1000 + b)
         s = base.stat.copy()
         s[:, :, 1 + base.N:] = zb.stat[:, :, 1 + base.N:]  # point b's inputs
         stat[:, b] = s.reshape(Q, top, 13)
