@@ -550,6 +550,12 @@ struct Plan {
         nrows_mine * nb16 * (nb16 + 1) / 2 >= (int64_t(1) << 31))
       return nl;
     if (conv_mode >= 2 || cta_mode()) return 0;  // waves, dataflow and CTA-local dataflow take every layer
+    // Short chains (d < 24): a layer's critical path is short, so band tasks
+    // have little to pipeline and add hand-out and flag costs -- layered wins
+    // (conv stage, layered vs dataflow: C1 = p1 d=15 m=2 0.070 vs 0.117 ms;
+    // p2 d=15 m=2 0.82 vs 1.40; p1 d=15 m=10 0.69 vs 0.92). At d=31 it is
+    // mixed (p1 m=10 2.14 vs 1.54, p2 m=2 1.49 vs 1.85), at d=63 banded wins.
+    if (d < 24) return nl;
     const int64_t thr = int64_t(sms) * 4 * 128 * 2, npairs = (d + 2) / 2;
     if (static_cast<int64_t>(batch) * layer_pairs < thr) return 0;
     int f = nl;
