@@ -219,7 +219,8 @@ double md_to_double(const double* limbs, int m, size_t stride) {  // multidouble
 // compares its sequential and parallel engines bit for bit, then both with
 // eval_direct; here the engine's distinct device paths are compared bit for
 // bit -- layered fused vs layered split convolutions, the dataflow and the
-// banded-wave schedules vs layered, the planner's own pick, a batch vs one
+// banded-wave schedules vs layered, the two CTA-local forms (band-task
+// dataflow, layer walk) vs layered, the planner's own pick, a batch vs one
 // point -- and the engine with the independent device evaluator
 // (pse_eval_direct: direct product chains, literal md arithmetic) within the
 // reference's tolerance 2^(32-52m) * max(1, |ref|).
@@ -234,8 +235,12 @@ int do_verify(const Prob& p, int device, const std::string& oracle_flag) {
   std::vector<double> split = eval_path(p, one, 1, device, "layer", huge);
   std::vector<double> flow = eval_path(p, one, 1, device, "flow", nullptr);
   std::vector<double> waves = eval_path(p, one, 1, device, "band", nullptr);
+  std::vector<double> cta = eval_path(p, one, 1, device, "cta", nullptr);
+  std::vector<double> ctl = eval_path(p, one, 1, device, "ctl", nullptr);
   std::vector<double> autop = eval_path(p, one, 1, device, nullptr, nullptr);
   perturb(fused, "fused", p);
+  perturb(cta, "cta", p);
+  perturb(ctl, "ctl", p);
   perturb(split, "split", p);
   perturb(flow, "flow", p);
   perturb(waves, "band", p);
@@ -257,6 +262,8 @@ int do_verify(const Prob& p, int device, const std::string& oracle_flag) {
   report("layered fused vs layered split convolutions", same(fused, split));
   report("dataflow (banded, one persistent launch) vs layered", same(flow, fused));
   report("banded waves vs layered", same(waves, fused));
+  report("CTA-local dataflow vs layered", same(cta, fused));
+  report("CTA-local layers vs layered", same(ctl, fused));
   report("planner's path vs layered", same(autop, fused));
   bool batch_ok = true;
   for (int q = 0; q < p.Q(); ++q)

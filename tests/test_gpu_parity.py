@@ -529,8 +529,8 @@ def test_plan_reused_across_batch_sizes():
 def test_cli_verify_and_bench(tmp_path):
     """pseval_b200 verify / bench (the reference CLI's subcommands over the
     device engine): verify compares the layered fused and split convolutions,
-    the dataflow and banded-wave schedules, the planner's path and a batch of
-    points bit for bit, and the engine with the independent device evaluator
+    the dataflow and banded-wave schedules, the two CTA-local forms, the
+    planner's path and a batch of points bit for bit, and the engine with the independent device evaluator
     within the reference's tolerance (pseval.cpp:97-118)."""
     import os
     import subprocess
@@ -541,7 +541,7 @@ def test_cli_verify_and_bench(tmp_path):
                  ["verify", "p2", "--degree", "20", "--precision", "3", "--oracle", "on"]):
         r = subprocess.run([cli, *args], capture_output=True, text=True, timeout=600)
         assert r.returncode == 0 and "verify: PASS" in r.stdout, r.stdout + r.stderr
-        assert r.stdout.count("bitwise equal") == 5, r.stdout
+        assert r.stdout.count("bitwise equal") == 7, r.stdout
         assert "oracle: independent device evaluator" in r.stdout and ": ok" in r.stdout, r.stdout
     path = str(tmp_path / "p2.txt")
     assert subprocess.run([cli, "gen", "p2", path, "--degree", "3", "--precision", "3"]).returncode == 0
@@ -559,6 +559,8 @@ def test_cli_verify_and_bench(tmp_path):
 @pytest.mark.parametrize("which,line", [("split", "layered fused vs layered split convolutions: MISMATCH"),
                                         ("flow", "dataflow (banded, one persistent launch) vs layered: MISMATCH"),
                                         ("band", "banded waves vs layered: MISMATCH"),
+                                        ("cta", "CTA-local dataflow vs layered: MISMATCH"),
+                                        ("ctl", "CTA-local layers vs layered: MISMATCH"),
                                         ("oracle", "max coefficient discrepancy")])
 def test_cli_verify_fails_on_a_broken_path(which, line):
     """verify is not vacuous: a one-ulp change in one path's result (or a
