@@ -193,13 +193,14 @@ struct CtaArgs {
 
 // CTA-local layered convolution (deep graphs of few large job groups at small
 // precisions): ONE block per independent job group and point runs the
-// group's conv layers in order, a block barrier between layers; within a
-// layer every thread takes whole coefficient pairs (k, d-k) of the layer's
-// jobs, as k_conv does. The operands were written earlier in the launch by
-// this block (or staged before it), so they are read through L1. A layer's
-// critical path is one pair's d+2 steps; at M = 1 a step is one DMUL + DADD,
-// so the 64 layers of p2 cost ~64 x (d+2) dependent DADDs -- no task
-// hand-out, no completion flags.
+// group's conv layers in order, a block barrier between layers -- no task
+// hand-out, no completion flags. At M >= 2 (only when forced) every thread
+// takes whole coefficient pairs (k, d-k) of the layer's jobs, as k_conv
+// does, reading operands this block wrote earlier through L1; at M = 1 (the
+// default there) the operands are staged in shared memory and every thread
+// runs a register block of adjacent chains (ctl_group_m1). A layer's
+// critical path is its longest chain: d+1 dependent steps, at M = 1 one
+// DMUL + DADD each.
 struct CtlArgs {
   double* arena;
   Geom G;
