@@ -166,6 +166,18 @@ def test_p1_bitwise_vs_sequential(d, m, conv_path):
     assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"p1 d={d} m={m}")
 
 
+@pytest.mark.parametrize("pid", ["p1", "p2", "p3"])
+@pytest.mark.parametrize("d", [0, 1, 2, 3, 5])
+def test_m1_small_degrees_default_path(pid, d):
+    """m=1 through the planner's default (the CTA-local layer walk: register
+    blocks of three chains, the last block partly past d) at degrees whose
+    chains are shorter than one block"""
+    p = po.gen_benchmark(pid, d, 1, seed=7)
+    ref = po.evaluate(p, "port")
+    vg, _ = dev_eval(p)
+    assert_bitwise(vg[:, 0].reshape(ref.shape), ref, f"{pid} d={d} m=1")
+
+
 @pytest.mark.parametrize("pid,d,m", [("p2", 3, 2), ("p3", 3, 2), ("p2", 8, 10), ("p3", 2, 10)])
 def test_p2_p3_bitwise(pid, d, m, conv_path):
     p = po.gen_benchmark(pid, d, m, seed=7)
