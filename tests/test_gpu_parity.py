@@ -278,18 +278,20 @@ def _p2h(p: po.Problem) -> po.Problem:
 
 
 @pytest.mark.parametrize("cfg,pid,m", [("C2", "p1", 10), ("C3", "p2", 10), ("C3'", "p2h", 10), ("C4", "p3", 10),
-                                       ("C3 m=2", "p2", 2), ("C3 m=5", "p2", 5)])
+                                       ("C3 m=1", "p2", 1), ("C3 m=2", "p2", 2), ("C3 m=5", "p2", 5),
+                                       ("C1", "p1", 2)])
 def test_benchmark_configs_full_size_bitwise_vs_reference_engine(cfg, pid, m):
-    """The BASELINE configurations at full size (d=152, seed 7) through the
-    conv path the planner picks for them (layered/hybrid for C2 and C4,
-    dataflow for C3 and C3'): value and every gradient series equal the
-    reference engine's run_parallel (oracle/_ref, the reference's own
-    sources) bit for bit."""
+    """The BASELINE configurations at full size (d=152, seed 7; C1 at d=15)
+    through the conv path the planner picks for them (layered/hybrid for C2
+    and C4, dataflow for C3 and C3', the CTA-local layer walk for C3 at m=1,
+    layered for C1): value and every gradient series equal the reference
+    engine's run_parallel (oracle/_ref, the reference's own sources) bit for
+    bit."""
     import os
 
     if not po.has_ref():
         pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
-    p = po.gen_benchmark("p2" if pid == "p2h" else pid, 152, m, seed=7)
+    p = po.gen_benchmark("p2" if pid == "p2h" else pid, 15 if cfg == "C1" else 152, m, seed=7)
     if pid == "p2h":
         p = _p2h(p)
     ref = po.evaluate(p, "ref", workers=os.cpu_count() or 1)
